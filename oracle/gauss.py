@@ -1,0 +1,182 @@
+"""Oracle sketch generator: Philox4x32-10 + the frozen RTK-GAUSS-1 Box-Muller.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The paper draws "a standard Gaussian matrix Omega_k" afresh for every mode
+(Alg. 3 line 3; Alg. 4 line 3; definition of a
+standard Gaussian matrix PAPER.md:96).  It names no generator, so this build
+freezes one (SURVEY.md 8(c) reading C2, restated in DESIGN.md "RTK-GAUSS-1"):
+
+  key     = (lo32(seed), hi32(seed))
+  counter = (c // 4, lo32(j), hi32(j), k)     j = canonical unfolding column,
+                                              c = sketch column, k = 1-based mode
+  x0..x3  = Philox4x32-10(counter, key)       (Salmon et al. 2011)
+  (x0,x1) -> Box-Muller pair -> columns 4*(c//4)+0, +1
+  (x2,x3) -> Box-Muller pair -> columns 4*(c//4)+2, +3
+  u       = ((x >> 8) + 0.5) * 2^-24          (exact in float64, u in (0,1))
+  z0      = sqrt(-2 ln u_a) cos(2 pi u_b),  z1 = sqrt(-2 ln u_a) sin(2 pi u_b)
+
+ln, sin and cos are evaluated with the fixed range reductions and fixed
+polynomials below using only IEEE-754 binary64 +, -, *, / and sqrt, each
+correctly rounded and never fused, in exactly the order written here.  The
+float64 Gaussian is rounded to float32 (round-to-nearest-even); Omega_k is that
+float32 value.  The CUDA side implements the same written spec independently
+(no shared code); the two must agree bit for bit.
+
+Pins (tests/test_oracle_gauss.py): Philox against an independently compiled
+cuRAND ``curand_Philox4x32_10`` and published known-answer vectors; ln/sin/cos
+against libm (numpy) to <= 4 ulp; moments and a KS test of the Gaussians.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+_M0 = np.uint64(0xD2511F53)
+_M1 = np.uint64(0xCD9E8D57)
+_W0 = np.uint64(0x9E3779B9)
+_W1 = np.uint64(0xBB67AE85)
+_MASK = np.uint64(0xFFFFFFFF)
+_S32 = np.uint64(32)
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Philox4x32 with 10 rounds (Salmon, Moraes, Dror, Shaw, SC'11).
+
+    Inputs are array-likes of uint32 values (broadcast together); returns four
+    uint32 arrays.  Round: (hi0,lo0)=M0*c0, (hi1,lo1)=M1*c2,
+    out=(hi1^c1^k0, lo1, hi0^c3^k1, lo0); key bumped by (W0,W1) between
+    rounds.
+    """
+    c0 = np.asarray(c0, dtype=np.uint64)
+    c1 = np.asarray(c1, dtype=np.uint64)
+    c2 = np.asarray(c2, dtype=np.uint64)
+    c3 = np.asarray(c3, dtype=np.uint64)
+    k0 = np.asarray(k0, dtype=np.uint64)
+    k1 = np.asarray(k1, dtype=np.uint64)
+    for rnd in range(10):
+        p0 = _M0 * c0
+        p1 = _M1 * c2
+        hi0, lo0 = p0 >> _S32, p0 & _MASK
+        hi1, lo1 = p1 >> _S32, p1 & _MASK
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+        if rnd < 9:
+            k0 = (k0 + _W0) & _MASK
+            k1 = (k1 + _W1) & _MASK
+    return (c0.astype(np.uint32), c1.astype(np.uint32),
+            c2.astype(np.uint32), c3.astype(np.uint32))
+
+
+# ---- RTK-GAUSS-1 constants (binary64, written as hex so both sides agree) ----
+LN2_HI = float.fromhex("0x1.62e42fee00000p-1")
+LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
+SQRT2 = float.fromhex("0x1.6a09e667f3bcdp+0")
+PIO2 = float.fromhex("0x1.921fb54442d18p+0")
+TWO_M23 = float.fromhex("0x1p-23")
+# ln: 2 s * sum_{k=0..11} z^k/(2k+1)
+LOG_C = [1.0 / (2 * k + 1) for k in range(12)]
+# sin: x * sum_{k=0..8} (-1)^k y^k/(2k+1)!    cos: sum_{k=0..9} (-1)^k y^k/(2k)!
+def _fact(n):
+    f = 1.0
+    for i in range(2, n + 1):
+        f = f * float(i)          # exact: every n! used here is < 2^53
+    return f
+SIN_C = [(-1.0 if k % 2 else 1.0) / _fact(2 * k + 1) for k in range(9)]
+COS_C = [(-1.0 if k % 2 else 1.0) / _fact(2 * k) for k in range(10)]
+
+
+def _odd_int(x):
+    """x (uint32) -> v = 2*(x>>8)+1, an odd integer in [1, 2^25); u = v*2^-25."""
+    return (np.asarray(x, dtype=np.uint64) >> np.uint64(8)) * np.uint64(2) + np.uint64(1)
+
+
+def uniform01(x):
+    """u = ((x>>8)+0.5)*2^-24, exact in binary64."""
+    return _odd_int(x).astype(np.float64) * float.fromhex("0x1p-25")
+
+
+def rtk_log_u(x):
+    """ln(u) for u = ((x>>8)+0.5)*2^-24 using the RTK-GAUSS-1 recipe.
+
+    v = 2(x>>8)+1 (odd, < 2^25); e = floor(log2 v); f = v*2^-e in [1,2) (exact);
+    if f > SQRT2: f = f/2, e = e+1 (exact);  s = (f-1)/(f+1); z = s*s;
+    p = Horner(LOG_C, z); lnf = (2*s)*p;  ln u = (e-25)*LN2_HI + ((e-25)*LN2_LO + lnf).
+    """
+    v = _odd_int(x)
+    # e = bit_length(v) - 1 = #{b in 1..24 : v >> b != 0}   (integer arithmetic)
+    e = np.zeros(v.shape, dtype=np.int64)
+    for b in range(1, 25):
+        e += ((v >> np.uint64(b)) != 0).astype(np.int64)
+    f = v.astype(np.float64) * np.ldexp(1.0, -e)
+    big = f > SQRT2
+    f = np.where(big, f * 0.5, f)
+    e = np.where(big, e + 1, e)
+    s = (f - 1.0) / (f + 1.0)
+    z = s * s
+    p = np.full_like(z, LOG_C[11])
+    for k in range(10, -1, -1):
+        p = p * z + LOG_C[k]
+    lnf = (2.0 * s) * p
+    n = (e - 25).astype(np.float64)
+    return n * LN2_HI + (n * LN2_LO + lnf)
+
+
+def rtk_sincos_2pi_u(x):
+    """(sin(2 pi u), cos(2 pi u)) for u = ((x>>8)+0.5)*2^-24, RTK-GAUSS-1 recipe.
+
+    w = 2(x>>8)+1; quadrant qd = w>>23; rem = w & (2^23-1); t = rem*2^-23 (exact);
+    if rem < 2^22: x = t*PIO2, (S,C) = (sin x, cos x)
+    else:          x = (1-t)*PIO2, (S,C) = (cos x, sin x)
+    sin x = x*Horner(SIN_C, x*x); cos x = Horner(COS_C, x*x);
+    quadrant: qd=0 -> (S,C); 1 -> (C,-S); 2 -> (-S,-C); 3 -> (-C,S)  as (sin,cos).
+    """
+    w = _odd_int(x)
+    qd = (w >> np.uint64(23)).astype(np.int64)
+    rem = w & np.uint64((1 << 23) - 1)
+    t = rem.astype(np.float64) * TWO_M23
+    low = rem < np.uint64(1 << 22)
+    xr = np.where(low, t, 1.0 - t) * PIO2
+    y = xr * xr
+    ps = np.full_like(y, SIN_C[8])
+    for k in range(7, -1, -1):
+        ps = ps * y + SIN_C[k]
+    sx = xr * ps
+    pc = np.full_like(y, COS_C[9])
+    for k in range(8, -1, -1):
+        pc = pc * y + COS_C[k]
+    cx = pc
+    S = np.where(low, sx, cx)
+    C = np.where(low, cx, sx)
+    sin_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [S, C, -S, -C])
+    cos_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [C, -S, -C, S])
+    return sin_o, cos_o
+
+
+def box_muller(xa, xb):
+    """RTK-GAUSS-1 pair: r = sqrt(-2*ln u_a); (r*cos(2 pi u_b), r*sin(2 pi u_b)) in float64."""
+    r = np.sqrt(-2.0 * rtk_log_u(xa))
+    s, c = rtk_sincos_2pi_u(xb)
+    return r * c, r * s
+
+
+def omega(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
+    """Rows [row0, row0+rows) of Omega_k (float32, shape rows x l).
+
+    Row index = canonical unfolding column j (Kolda-Bader order, SURVEY.md 8(c)
+    C3); mode = 1-based mode index k in processing order.  Follows PAPER.md:257
+    ("Draw a standard Gaussian matrix Omega_k") with the RTK-GAUSS-1 stream.
+    """
+    j = np.arange(row0, row0 + rows, dtype=np.uint64)
+    n4 = (l + 3) // 4
+    jj = j[:, None]
+    c4 = np.arange(n4, dtype=np.uint64)[None, :]
+    k0 = np.uint64(seed & 0xFFFFFFFF)
+    k1 = np.uint64((seed >> 32) & 0xFFFFFFFF)
+    x0, x1, x2, x3 = philox4x32_10(c4, jj & _MASK, jj >> _S32, np.uint64(mode), k0, k1)
+    z0, z1 = box_muller(x0, x1)
+    z2, z3 = box_muller(x2, x3)
+    out = np.empty((rows, n4 * 4), dtype=np.float64)
+    out[:, 0::4] = z0
+    out[:, 1::4] = z1
+    out[:, 2::4] = z2
+    out[:, 3::4] = z3
+    return out[:, :l].astype(np.float32)

@@ -1,0 +1,251 @@
+"""Pins for the float64 oracle (oracle/tucker.py, oracle/metrics.py) - CPU only.
+
+Each test pins the oracle to something other than itself: brute-force index
+loops, direct summation, closed forms from the paper (Thm 2.2 PAPER.md:131-142,
+Eq. (3.2), tensor B's spectrum PAPER.md:806-815), exact
+recovery (north_star), the shift invariants of PAPER.md:272-289,
+and convergence to deterministic T-/ST-HOSVD (Alg. 1).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import metrics, tucker
+from workloads import make_config_tensor, orthonormal_factor, tucker_tensor
+
+
+def rnd(shape, seed=0):
+    return np.random.default_rng(seed).standard_normal(shape)
+
+
+# --------------------------------------------------------------- tensor ops
+@pytest.mark.parametrize("dims", [(2, 3, 4), (3, 1, 2, 5), (4, 5)])
+def test_unfold_matches_kolda_bader_index(dims):
+    t = rnd(dims, 1)
+    d = len(dims)
+    for k in range(d):
+        m = tucker.unfold(t, k)
+        assert m.shape == (dims[k], int(np.prod(dims)) // dims[k])
+        for idx in itertools.product(*[range(n) for n in dims]):
+            j, stride = 0, 1
+            for mm in range(d):
+                if mm == k:
+                    continue
+                j += idx[mm] * stride
+                stride *= dims[mm]
+            assert m[idx[k], j] == t[idx]
+        np.testing.assert_array_equal(tucker.fold(m, k, dims), t)
+
+
+def test_mode_product_direct_summation():
+    t = rnd((4, 5, 6), 2)
+    b = rnd((3, 5), 3)
+    out = tucker.mode_product(t, b, 1)
+    ref = np.zeros((4, 3, 6))
+    for i in range(4):
+        for jj in range(3):
+            for k in range(6):
+                ref[i, jj, k] = sum(t[i, x, k] * b[jj, x] for x in range(5))
+    np.testing.assert_allclose(out, ref, rtol=1e-13, atol=1e-13)
+
+
+def test_mode_products_commute_and_isometry():
+    t = rnd((4, 5, 6), 4)
+    b, c = rnd((3, 4), 5), rnd((2, 6), 6)
+    x = tucker.mode_product(tucker.mode_product(t, b, 0), c, 2)
+    y = tucker.mode_product(tucker.mode_product(t, c, 2), b, 0)
+    np.testing.assert_allclose(x, y, rtol=1e-13, atol=1e-13)
+    q = orthonormal_factor(5, 5, np.random.default_rng(0))
+    assert abs(np.linalg.norm(tucker.mode_product(t, q.T, 1)) - np.linalg.norm(t)) < 1e-12
+
+
+def test_sign_pin():
+    u = np.array([[0.1, -0.9, 0.5], [-0.8, 0.2, -0.5], [0.3, 0.1, 0.0]])
+    v = tucker.sign_pin(u)
+    np.testing.assert_array_equal(v[:, 0], -u[:, 0])   # |-0.8| largest, negative -> flip
+    np.testing.assert_array_equal(v[:, 1], -u[:, 1])   # -0.9
+    np.testing.assert_array_equal(v[:, 2], u[:, 2])    # tie 0.5/-0.5: lowest index (+) wins
+
+
+# ------------------------------------------------------------ RE evaluator
+def test_relative_error_direct_reconstruction():
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((6, 7, 5))
+    core = rng.standard_normal((3, 4, 2))
+    us = [orthonormal_factor(n, r, rng) for n, r in zip((6, 7, 5), (3, 4, 2))]
+    rec = np.einsum("abc,ia,jb,kc->ijk", core, *us)
+    ref = np.linalg.norm(a - rec) / np.linalg.norm(a)
+    assert abs(metrics.relative_error(a, core, us) - ref) < 1e-14
+    assert abs(metrics.relative_error(a, np.zeros_like(core), us) - 1.0) < 1e-15
+
+
+def test_principal_angle_known_rotation():
+    th = 0.3
+    u = np.array([[1.0, 0], [0, 1], [0, 0]])
+    v = np.array([[1.0, 0], [0, np.cos(th)], [0, np.sin(th)]])
+    assert abs(metrics.max_principal_angle(u, v) - th) < 1e-14
+    assert metrics.max_principal_angle(u, u @ np.array([[0.6, 0.8], [-0.8, 0.6]])) < 1e-15
+
+
+# -------------------------------------------------------------- Algorithm 1
+def _tensor_b(n, v, seed):
+    """Tensor B of PAPER.md:806-815 at desk scale: tendiag(v) x_k A_k."""
+    rng = np.random.default_rng(seed)
+    d = np.zeros((n, n, n))
+    for i in range(n):
+        d[i, i, i] = v[i]
+    us = [orthonormal_factor(n, n, rng) for _ in range(3)]
+    return np.einsum("abc,ia,jb,kc->ijk", d, *us)
+
+
+def test_thosvd_tensor_b_closed_form():
+    n, r = 12, 4
+    v = np.exp(-np.arange(1, n + 1) / 3.0)          # 'fast decay' family
+    b = _tensor_b(n, v, 3)
+    for seq in (False, True):
+        core, us = tucker.thosvd(b, (r, r, r), sequential=seq)
+        re2 = metrics.relative_error(b, core, us) ** 2
+        # sigma(B_(k)) = sorted v; the exact HOSVD of a diagonal core keeps
+        # exactly the r x r x r diagonal block: RE^2 = sum_{i>r} v_i^2 / sum v_i^2
+        closed = np.sum(v[r:] ** 2) / np.sum(v ** 2)
+        assert abs(re2 - closed) < 1e-12
+        for k in range(3):
+            s = np.linalg.svd(tucker.unfold(b, k), compute_uv=False)
+            np.testing.assert_allclose(s, np.sort(v)[::-1], rtol=1e-11, atol=1e-14)
+
+
+def test_thosvd_theorem_2_2():
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((7, 8, 6)) + tucker_tensor(rng.standard_normal((3, 3, 3)),
+                                                      [orthonormal_factor(n, 3, rng) for n in (7, 8, 6)],
+                                                      dtype=np.float64) * 10
+    ranks = (3, 4, 2)
+    tails = []
+    for k, r in enumerate(ranks):
+        s = np.linalg.svd(tucker.unfold(a, k), compute_uv=False)
+        tails.append(np.sum(s[r:] ** 2))
+    for seq in (False, True):
+        core, us = tucker.thosvd(a, ranks, sequential=seq)
+        err2 = (metrics.relative_error(a, core, us) * np.linalg.norm(a)) ** 2
+        assert err2 <= sum(tails) * (1 + 1e-12)
+        if not seq:
+            # per-mode equality ||A x_k (I - U U^T)||^2 = tail energy (Thm 2.2)
+            for k, u in enumerate(us):
+                m = tucker.unfold(a, k)
+                res = np.sum((m - u @ (u.T @ m)) ** 2)
+                assert abs(res - tails[k]) <= 1e-10 * tails[k]
+
+
+def test_st_identity_and_orthonormality():
+    """||A - A_hat||^2 = sum_k discarded energies = ||A||^2 - ||G||^2 (Eq. 3.2 structure)."""
+    rng = np.random.default_rng(10)
+    a = rng.standard_normal((9, 8, 7, 6))
+    res = tucker.rsthosvd(a, (3, 4, 2, 3), p=2, q=2, seed=11)
+    err2 = (metrics.relative_error(a, res.core, res.factors) * np.linalg.norm(a)) ** 2
+    disc = metrics.st_discarded_energies(a, res.factors)
+    assert abs(err2 - sum(disc)) <= 1e-12 * np.sum(a ** 2)
+    assert abs(err2 - (np.sum(a ** 2) - np.sum(res.core ** 2))) <= 1e-12 * np.sum(a ** 2)
+    for u in res.factors:
+        assert metrics.orthonormality(u) <= 1e-12
+
+
+# ------------------------------------------------------------ Algorithms 3/4
+def _exact_tucker(dims, ranks, seed):
+    rng = np.random.default_rng(seed)
+    core = rng.standard_normal(ranks)
+    us = [orthonormal_factor(n, r, rng) for n, r in zip(dims, ranks)]
+    return tucker_tensor(core, us, dtype=np.float64)
+
+
+@pytest.mark.parametrize("algo", ["rthosvd", "rsthosvd"])
+@pytest.mark.parametrize("dims,ranks,p", [((20, 18, 16), (3, 4, 2), 3), ((12, 10, 9, 8), (2, 3, 2, 2), 2),
+                                          ((30, 25), (4, 5), 4)])
+def test_exact_recovery(algo, dims, ranks, p):
+    a = _exact_tucker(dims, ranks, 12)
+    res = getattr(tucker, algo)(a, ranks, p=p, q=1, seed=13)
+    assert metrics.relative_error(a, res.core, res.factors) <= 1e-10
+    for u in res.factors:
+        assert metrics.orthonormality(u) <= 1e-12
+
+
+@pytest.mark.parametrize("seq", [False, True])
+def test_converges_to_deterministic_hosvd(seq):
+    """Gapped tiny tensor, large q: randomized factors -> Alg. 1 factors."""
+    rng = np.random.default_rng(14)
+    dims, ranks = (16, 14, 12), (3, 3, 3)
+    core = np.zeros((6, 6, 6))
+    for i in range(6):
+        core[i, i, i] = [10.0, 8.0, 6.0, 1.0, 0.5, 0.25][i]
+    us = [orthonormal_factor(n, 6, rng) for n in dims]
+    a = tucker_tensor(core, us, noise=1e-3, rng=rng, dtype=np.float64)
+    det_core, det_us = tucker.thosvd(a, ranks, sequential=seq)
+    fn = tucker.rsthosvd if seq else tucker.rthosvd
+    res = fn(a, ranks, p=2, q=40, seed=15)
+    for u_d, u_r in zip(det_us, res.factors):
+        assert metrics.max_principal_angle(u_d, u_r) <= 1e-10
+        np.testing.assert_allclose(u_r, u_d, atol=1e-9)          # sign pin makes them equal
+    np.testing.assert_allclose(res.core, det_core, atol=1e-8)
+
+
+def test_shift_closed_form_rank_l():
+    """If rank(M) = l the sketch spans the dominant invariant subspace, so
+    Sigma(Y_t) = lambda_i - alpha and alpha_t = lambda_l/2 for every t >= 1
+    (SURVEY 8(c) alpha pin).  A dropped or sign-flipped
+    alpha*Q term breaks the second step."""
+    rng = np.random.default_rng(16)
+    n, m, l = 20, 30, 5
+    m_mat = rng.standard_normal((n, l)) @ rng.standard_normal((l, m))
+    lam = np.sort(np.linalg.eigvalsh(m_mat @ m_mat.T))[::-1]
+    u, tr = tucker._range_finder(m_mat, r=3, p=2, q=5, seed=17, mode1=1, shift=True)
+    for a_t in tr.alpha:
+        assert abs(a_t - lam[l - 1] / 2) <= 1e-10 * lam[l - 1]
+
+
+def test_shift_invariants_random():
+    """alpha never decreases and never exceeds lambda_l(M M^T)/2."""
+    viol = 0
+    for s in range(30):
+        rng = np.random.default_rng(100 + s)
+        n, m = int(rng.integers(8, 20)), int(rng.integers(20, 60))
+        sv = np.exp(-rng.uniform(0.05, 0.6) * np.arange(n))
+        mm = orthonormal_factor(n, n, rng) @ np.diag(sv) @ orthonormal_factor(m, n, rng).T
+        r, p = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        lam = np.sort(np.linalg.eigvalsh(mm @ mm.T))[::-1]
+        _, tr = tucker._range_finder(mm, r, p, q=6, seed=s, mode1=1, shift=True)
+        al = [0.0] + tr.alpha
+        assert all(b >= a for a, b in zip(al, al[1:]))
+        viol += sum(a > lam[r + p - 1] / 2 * (1 + 1e-12) for a in tr.alpha)
+        assert tr.alpha[-1] > 0
+    assert viol == 0
+
+
+def test_alpha_zero_is_algorithm_2():
+    """shift=False keeps alpha at 0 (Alg. 2); it is less accurate than the shift on a
+    slowly decaying spectrum at equal q (PAPER.md:289 claim, median over seeds)."""
+    rng = np.random.default_rng(18)
+    dims = (30, 30, 30)
+    sv = 1.0 / np.arange(1, 31) ** 1.0
+    core = np.zeros((30, 30, 30))
+    for i in range(30):
+        core[i, i, i] = sv[i]
+    a = tucker_tensor(core, [orthonormal_factor(30, 30, rng) for _ in range(3)], dtype=np.float64)
+    re_s, re_0 = [], []
+    for s in range(9):
+        r1 = tucker.rsthosvd(a, (5, 5, 5), p=2, q=1, seed=s, shift=True)
+        r0 = tucker.rsthosvd(a, (5, 5, 5), p=2, q=1, seed=s, shift=False)
+        assert all(x == 0.0 for t in r0.traces for x in t.alpha)
+        re_s.append(metrics.relative_error(a, r1.core, r1.factors))
+        re_0.append(metrics.relative_error(a, r0.core, r0.factors))
+    assert np.median(re_s) <= np.median(re_0) * 1.0 + 1e-15
+
+
+def test_config_c1_oracle_ballpark():
+    """C1 at full size: RE equals deterministic T-HOSVD's (gaps ~98%)."""
+    a = make_config_tensor("c1")
+    res = tucker.rthosvd(a, (5, 5, 5), p=5, q=2, seed=1002)
+    det_core, det_us = tucker.thosvd(a.astype(np.float64), (5, 5, 5), sequential=False)
+    re = metrics.relative_error(a, res.core, res.factors)
+    re_det = metrics.relative_error(a, det_core, det_us)
+    assert abs(re - re_det) <= 1e-6 * re_det
+    assert 0.02 < re < 0.08
