@@ -1,0 +1,136 @@
+/*
+ * rtucker.h -- C ABI of the B200-native adaptive-shift randomized Tucker hot path.
+ *
+ * Implements the per-mode randomized range finder with adaptive shifted power
+ * iteration of Che, Wei, Wu, Yan, arXiv 2506.04840:
+ *   Alg. 3 "shifted randomized T-HOSVD"   PAPER.md:250-270   -> rtk_rthosvd
+ *   Alg. 4 "shifted randomized ST-HOSVD"  PAPER.md:293-313   -> rtk_rsthosvd
+ *   Alg. 2 (alpha = 0) and Alg. B.1 (PVE stop,
+ *   PAPER.md:1145-1172) through rtk_solve() options.
+ * Per mode k (order 1..d): Omega_k (RTK-GAUSS-1),
+ * Y = M Omega_k, Q = orth(Y), alpha = 0; q times { Y = M (M^T Q) - alpha Q;
+ * [Q,Sigma] = svd(Y); if Sigma(l,l) > alpha: alpha = (Sigma(l,l)+alpha)/2 };
+ * U_k = Q(:,1:r_k) (sign-pinned); M = A_(k) (Alg. 3) or G_(k) (Alg. 4), and
+ * Alg. 4 shrinks G = G x_k U_k^T after each mode.
+ *
+ * LAYOUT.  All tensors are float32, COLUMN-MAJOR (mode-1 index fastest; the
+ * MATLAB / Kolda-Bader convention):  A[i_1 + n_1 (i_2 + n_2 (...))].
+ * That is the same byte layout as a C-contiguous torch tensor of shape
+ * (n_d, ..., n_1).  U[k] is n_k x r_k column-major (leading dimension n_k).
+ * core is r_1 x ... x r_d column-major.  A, U[k] and core are DEVICE pointers.
+ *
+ * OWNERSHIP.  The caller allocates and owns A, every U[k], core and ws; the
+ * library never frees them and never writes A.  The library keeps no state
+ * between calls except a per-thread error string and cached kernel attributes.
+ * If ws == NULL the call allocates (cudaMallocAsync) and frees its own
+ * workspace on the stream.
+ *
+ * EXECUTION.  Asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ * stream).  Outputs are valid once the stream is synchronised.  If `rep` is
+ * non-NULL the call synchronises the stream and fills the report.
+ *
+ * ERRORS.  Every function returns an rtk_status; nothing throws across the ABI.
+ * All argument checks run before any launch; on a non-zero status no output is
+ * written.  rtk_last_error() returns a thread-local message for the last
+ * non-zero status of this thread.
+ */
+#ifndef RTUCKER_H
+#define RTUCKER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RTK_API __attribute__((visibility("default")))
+#else
+#define RTK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rtk_status {
+  RTK_OK = 0,
+  RTK_ERR_ARG = 1,       /* NULL pointer; d < 2 or d > 8; n_k < 1; r_k not in [1,n_k]; p < 0; q < 1 */
+  RTK_ERR_SHAPE = 2,     /* l_k = r_k + p > min(n_k, m_k), or n_k > 2048 (kernel limit) */
+  RTK_ERR_ALIGN = 3,     /* A not 4-byte aligned */
+  RTK_ERR_WORKSPACE = 4, /* ws_bytes < rtk_workspace_bytes(...) */
+  RTK_ERR_CUDA = 5,      /* launch / runtime error; message kept */
+  RTK_ERR_NUMERIC = 6    /* non-finite iterate or unrepairable Cholesky breakdown (reported via rep) */
+} rtk_status;
+
+/* Optional host-side report (SPEC ShiftTrace analogue).  Any pointer may be NULL. */
+typedef struct rtk_report {
+  double* alpha_trace;  /* [d * q] : alpha after power step t of mode k at [k*q + t]     */
+  double* sigma;        /* [d * 128]: final diag(Sigma_k)+alpha of mode k at [k*128 + i] */
+  int32_t* q_used;      /* [d]   : power steps actually taken (== q unless PVE stopped)  */
+  int32_t fallback;     /* out   : # of rank-deficient basis completions performed        */
+  int32_t numeric;      /* out   : 0 ok, else RTK_ERR_NUMERIC                              */
+} rtk_report;
+
+/* Solver options for rtk_solve (defaults: {1, 1, 0.0, 0}). */
+typedef struct rtk_options {
+  int32_t sequential; /* 0: T-HOSVD (Alg. 3, every mode factors A_(k)); 1: ST-HOSVD (Alg. 4) */
+  int32_t shift;      /* 1: adaptive shift (Alg. 3/4); 0: alpha == 0 (Alg. 2)                */
+  double pve_tol;     /* > 0: Alg. B.1 PVE stop per mode with q as q_max (ST only)           */
+  int32_t path;       /* 0: auto, 1: FP32 FFMA tiles (other values reserved)                 */
+} rtk_options;
+
+/*
+ * Shifted randomized T-HOSVD, Alg. 3.
+ *   A      device, float32, column-major n_1 x ... x n_d, 4-byte aligned (16-byte and
+ *          n_1 % 4 == 0 select the fast vector loader; otherwise a scalar loader)
+ *   dims   host, d entries n_k >= 1;   d in [2, 8]
+ *   ranks  host, d entries r_k in [1, n_k]
+ *   p      oversampling s_k (same for all modes), l_k = r_k + p
+ *   q      power steps >= 1
+ *   seed   Omega seed (RTK-GAUSS-1 key); mode k uses counter word 3 = k (1-based)
+ *   U      host array of d DEVICE pointers, U[k] -> n_k x r_k float32 (written)
+ *   core   device, r_1 x ... x r_d float32 (written); core = A x_1 U_1^T ... x_d U_d^T
+ *   ws     device workspace of ws_bytes (>= rtk_workspace_bytes), or NULL
+ *   stream cudaStream_t
+ *   rep    optional host report (NULL: fully asynchronous)
+ */
+RTK_API int rtk_rthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+                int32_t p, int32_t q, uint64_t seed, float* const* U, float* core,
+                void* ws, size_t ws_bytes, void* stream, rtk_report* rep);
+
+/* Shifted randomized ST-HOSVD, Alg. 4, processing order 1..d.
+ * Arguments as rtk_rthosvd; core = G after the last shrink G = G x_d U_d^T. */
+RTK_API int rtk_rsthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+                 int32_t p, int32_t q, uint64_t seed, float* const* U, float* core,
+                 void* ws, size_t ws_bytes, void* stream, rtk_report* rep);
+
+/* General entry: Alg. 2 / 3 / 4 / B.1 selected by *opt (NULL -> ST-HOSVD, shift on). */
+RTK_API int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32_t d,
+              const int32_t* ranks, int32_t p, int32_t q, uint64_t seed, float* const* U,
+              float* core, void* ws, size_t ws_bytes, void* stream, rtk_report* rep);
+
+/* Workspace bytes for (algo: 0 = T-HOSVD, 1 = ST-HOSVD).  Returns 0 on invalid
+ * arguments (message in rtk_last_error()). */
+RTK_API size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks,
+                           int32_t p, int32_t q);
+
+/* Test hook: rows [row0, row0+rows) of Omega_mode (l columns) in RTK-GAUSS-1,
+ * written row-major to the DEVICE buffer out[(j-row0)*l + c] (float32). */
+RTK_API int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out,
+              void* stream);
+
+/* Test hook: one fused power step Y = M (M^T Q) on the column-major n x m matrix M (ld)
+ * with Q (n x l, column-major, ld n; device, float32); Y (n x l, column-major fp64, device).
+ * No shift, no orthonormalisation: exercises the streaming kernel alone. */
+RTK_API int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float* Q, int32_t l,
+                   double* Y, void* stream);
+
+/* Thread-local message for the last non-zero status. */
+RTK_API const char* rtk_last_error(void);
+
+/* Library version string, "rtucker <semver> sm_100a". */
+RTK_API const char* rtk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTUCKER_H */

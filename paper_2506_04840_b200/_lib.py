@@ -1,0 +1,242 @@
+"""ctypes binding of include/rtucker.h (argument marshalling only)."""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_omega",
+                 "rtk_power_step", "rtk_last_error", "rtk_version"]
+
+RTK_STATUS = {0: "RTK_OK", 1: "RTK_ERR_ARG", 2: "RTK_ERR_SHAPE", 3: "RTK_ERR_ALIGN",
+              4: "RTK_ERR_WORKSPACE", 5: "RTK_ERR_CUDA", 6: "RTK_ERR_NUMERIC"}
+
+
+class RtkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{RTK_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("alpha_trace", ctypes.POINTER(ctypes.c_double)),
+                ("sigma", ctypes.POINTER(ctypes.c_double)),
+                ("q_used", ctypes.POINTER(ctypes.c_int32)),
+                ("fallback", ctypes.c_int32),
+                ("numeric", ctypes.c_int32)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("sequential", ctypes.c_int32), ("shift", ctypes.c_int32),
+                ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32)]
+
+
+def lib_path() -> str:
+    return os.environ.get("RTUCKER_LIB", os.path.join(HERE, "librtucker.so"))
+
+
+def load_library():
+    """Load librtucker.so (raises loudly if it is missing: there is no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"rtucker CUDA library not built: {path} "
+                          "(run `python -m paper_2506_04840_b200.build`)")
+    lib = ctypes.CDLL(path)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    vp = ctypes.c_void_p
+    solver_args = [vp, i64p, ctypes.c_int32, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                   ctypes.POINTER(ctypes.c_void_p), vp, vp, ctypes.c_size_t, vp,
+                   ctypes.POINTER(_Report)]
+    lib.rtk_rthosvd.argtypes = solver_args
+    lib.rtk_rsthosvd.argtypes = solver_args
+    lib.rtk_solve.argtypes = [ctypes.POINTER(_Options)] + solver_args
+    for f in (lib.rtk_rthosvd, lib.rtk_rsthosvd, lib.rtk_solve):
+        f.restype = ctypes.c_int
+    lib.rtk_workspace_bytes.argtypes = [ctypes.c_int32, i64p, ctypes.c_int32, i32p, ctypes.c_int32,
+                                        ctypes.c_int32]
+    lib.rtk_workspace_bytes.restype = ctypes.c_size_t
+    lib.rtk_omega.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                              ctypes.c_int32, vp, vp]
+    lib.rtk_omega.restype = ctypes.c_int
+    lib.rtk_power_step.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, vp,
+                                   ctypes.c_int32, vp, vp]
+    lib.rtk_power_step.restype = ctypes.c_int
+    lib.rtk_last_error.restype = ctypes.c_char_p
+    lib.rtk_version.restype = ctypes.c_char_p
+    _LIB = lib
+    return lib
+
+
+def version() -> str:
+    return load_library().rtk_version().decode()
+
+
+def _check(code: int):
+    if code != 0:
+        msg = load_library().rtk_last_error().decode()
+        raise RtkError(code, msg)
+
+
+def _stream_handle(device):
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def as_column_major(x):
+    """Return x (shape n_1..n_d) with column-major strides (mode-1 fastest), copying if needed."""
+    import torch
+    d = x.dim()
+    rev = list(range(d - 1, -1, -1))
+    return x.permute(*rev).contiguous().permute(*rev)
+
+
+def _is_column_major(x) -> bool:
+    s = 1
+    for k in range(x.dim()):
+        if x.shape[k] != 1 and x.stride(k) != s:
+            return False
+        s *= x.shape[k]
+    return True
+
+
+def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int) -> int:
+    lib = load_library()
+    d = len(dims)
+    dd = (ctypes.c_int64 * d)(*dims)
+    rr = (ctypes.c_int32 * d)(*ranks)
+    n = lib.rtk_workspace_bytes(1 if sequential else 0, dd, d, rr, p, q)
+    if n == 0:
+        raise RtkError(1, lib.rtk_last_error().decode())
+    return int(n)
+
+
+@dataclass
+class Report:
+    alpha_trace: list      # d lists of q alphas
+    sigma: list            # d lists of l final sigma estimates (diag(Sigma)+alpha)
+    q_used: list
+    fallback: int
+    numeric: int
+
+
+class _WorkspaceCache:
+    """Keeps one device workspace per (device, size) so repeated solves do not reallocate."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, device, nbytes):
+        import torch
+        key = str(device)
+        b = self.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self.buf[key] = b
+        return b
+
+
+_WS = _WorkspaceCache()
+
+
+def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: bool = True,
+          report: bool = False, out=None, workspace=None):
+    """General solver: Alg. 4 (sequential) / Alg. 3 (not sequential); shift=False is Alg. 2.
+
+    Returns (core, [U_1..U_d]) or (core, U, Report) with report=True.
+    ``out=(core, [U_k])`` reuses caller-allocated outputs (column-major).
+    """
+    import torch
+    lib = load_library()
+    if not isinstance(A, torch.Tensor) or not A.is_cuda:
+        raise ValueError("A must be a CUDA torch.Tensor (no CPU fallback)")
+    if A.dtype != torch.float32:
+        raise ValueError("A must be float32")
+    if not _is_column_major(A):
+        raise ValueError("A must be column-major (mode-1 fastest); use as_column_major(A)")
+    dims = [int(s) for s in A.shape]
+    d = len(dims)
+    ranks = [int(r) for r in ranks]
+    if len(ranks) != d:
+        raise ValueError("len(ranks) must equal A.dim()")
+    dev = A.device
+    if out is None:
+        U = [torch.empty((r, n), dtype=torch.float32, device=dev).t() for n, r in zip(dims, ranks)]
+        core = as_column_major(torch.empty(ranks, dtype=torch.float32, device=dev))
+    else:
+        core, U = out
+    dd = (ctypes.c_int64 * d)(*dims)
+    rr = (ctypes.c_int32 * d)(*ranks)
+    up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
+    ws_bytes = workspace_bytes(sequential, dims, ranks, p, q) if min(ranks) >= 1 else 0
+    ws = workspace if workspace is not None else _WS.get(dev, max(ws_bytes, 1))
+    opt = _Options(1 if sequential else 0, 1 if shift else 0, 0.0, 0)
+    rep = None
+    bufs = None
+    if report:
+        at = (ctypes.c_double * (d * q))()
+        sg = (ctypes.c_double * (d * 128))()
+        qu = (ctypes.c_int32 * d)()
+        rep = _Report(ctypes.cast(at, ctypes.POINTER(ctypes.c_double)),
+                      ctypes.cast(sg, ctypes.POINTER(ctypes.c_double)),
+                      ctypes.cast(qu, ctypes.POINTER(ctypes.c_int32)), 0, 0)
+        bufs = (at, sg, qu)
+    with torch.cuda.device(dev):
+        code = lib.rtk_solve(ctypes.byref(opt), ctypes.c_void_p(A.data_ptr()), dd, d, rr, p, q,
+                             ctypes.c_uint64(seed), up, ctypes.c_void_p(core.data_ptr()),
+                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_handle(dev),
+                             ctypes.byref(rep) if rep is not None else None)
+    _check(code)
+    if not report:
+        return core, U
+    at, sg, qu = bufs
+    ls = [r + p for r in ranks]
+    r_obj = Report([list(at[k * q:(k + 1) * q]) for k in range(d)],
+                   [list(sg[k * 128:k * 128 + ls[k]]) for k in range(d)],
+                   list(qu), rep.fallback, rep.numeric)
+    return core, U, r_obj
+
+
+def rthosvd(A, ranks, p: int, q: int, seed: int, **kw):
+    """Shifted randomized T-HOSVD, Alg. 3 -> rtk_rthosvd semantics."""
+    return solve(A, ranks, p, q, seed, sequential=False, **kw)
+
+
+def rsthosvd(A, ranks, p: int, q: int, seed: int, **kw):
+    """Shifted randomized ST-HOSVD, Alg. 4 -> rtk_rsthosvd semantics."""
+    return solve(A, ranks, p, q, seed, sequential=True, **kw)
+
+
+def omega(seed: int, mode: int, row0: int, rows: int, l: int, device="cuda"):
+    """Rows [row0, row0+rows) of Omega_mode (RTK-GAUSS-1) computed by the CUDA kernel."""
+    import torch
+    lib = load_library()
+    out = torch.empty((rows, l), dtype=torch.float32, device=device)
+    with torch.cuda.device(out.device):
+        _check(lib.rtk_omega(ctypes.c_uint64(seed), mode, row0, rows, l,
+                             ctypes.c_void_p(out.data_ptr()), _stream_handle(out.device)))
+    return out
+
+
+def power_step(M, Q):
+    """Y = M (M^T Q) by the fused streaming kernel (test hook).  M: n x m column-major
+    float32 CUDA (stride(0) == 1), Q: n x l float32 CUDA; returns Y n x l float64."""
+    import torch
+    lib = load_library()
+    n, m = M.shape
+    if M.stride(0) != 1 or M.dtype != torch.float32 or not M.is_cuda:
+        raise ValueError("M must be a column-major float32 CUDA matrix")
+    ld = M.stride(1) if m > 1 else n
+    l = Q.shape[1]
+    Qc = Q.t().contiguous()                     # column-major n x l, ld n
+    Y = torch.empty((l, n), dtype=torch.float64, device=M.device)
+    with torch.cuda.device(M.device):
+        _check(lib.rtk_power_step(ctypes.c_void_p(M.data_ptr()), n, m, ld, ctypes.c_void_p(Qc.data_ptr()),
+                                  l, ctypes.c_void_p(Y.data_ptr()), _stream_handle(M.device)))
+    return Y.t()

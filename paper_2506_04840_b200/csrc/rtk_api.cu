@@ -1,0 +1,394 @@
+// rtk_api.cu -- C ABI (include/rtucker.h): validation, planning, workspace carving and
+// the per-mode launch sequence of Alg. 3 / Alg. 4.
+//
+// Host control only: every arithmetic step runs in the kernels of rtk_tile.cu /
+// rtk_small.cu.  Nothing is copied back to the host during a solve (alpha lives in
+// device memory), so the sequence is stream-ordered and CUDA-graph capturable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rtucker.h"
+#include "rtk_internal.h"
+
+namespace rtk {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+constexpr int kLMaxApi = 96;
+constexpr int kNMax = 4096;
+constexpr int kRB = 16;
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+int64_t pad4(int64_t n) { return (n + 3) / 4 * 4; }
+
+struct Problem {
+  int d = 0;
+  std::vector<int64_t> dims;
+  std::vector<int> ranks;
+  int p = 0, q = 0;
+  bool seq = true;
+};
+
+// m_k: columns of the matrix mode k factors (PAPER.md:257 vs :300)
+int64_t mode_cols(const Problem& P, int k) {
+  int64_t m = 1;
+  for (int j = 0; j < P.d; ++j) {
+    if (j == k) continue;
+    m *= (P.seq && j < k) ? P.ranks[j] : P.dims[j];
+  }
+  return m;
+}
+
+int validate(const Problem& P) {
+  if (P.d < 2 || P.d > 8) return fail(RTK_ERR_ARG, "d must be in [2, 8]");
+  for (int k = 0; k < P.d; ++k) {
+    if (P.dims[k] < 1) return fail(RTK_ERR_ARG, "dims[k] must be >= 1");
+    if (P.ranks[k] < 1 || P.ranks[k] > P.dims[k]) return fail(RTK_ERR_ARG, "ranks[k] must be in [1, n_k]");
+  }
+  if (P.p < 0) return fail(RTK_ERR_ARG, "oversampling p must be >= 0");
+  if (P.q < 1) return fail(RTK_ERR_ARG, "power parameter q must be >= 1 (PAPER.md:253)");
+  for (int k = 0; k < P.d; ++k) {
+    const int64_t l = (int64_t)P.ranks[k] + P.p;
+    const int64_t m = mode_cols(P, k);
+    if (l > P.dims[k] || l > m)
+      return fail(RTK_ERR_SHAPE, "l_k = r_k + p exceeds min(n_k, m_k) in mode " + std::to_string(k + 1) +
+                                     " (PAPER.md:272)");
+    if (l > kLMaxApi) return fail(RTK_ERR_SHAPE, "l_k > 96 is not supported by the one-CTA small solves");
+    if (P.dims[k] > kNMax) return fail(RTK_ERR_SHAPE, "n_k > 4096 is not supported by the tile kernels");
+  }
+  return RTK_OK;
+}
+
+// Views: the range-finder matrix of mode k, and the shrink input of mode k.
+View range_view(const Problem& P, int k, const float* A, const float* buf) {
+  View v;
+  v.n = (int)P.dims[k];
+  if (!P.seq || k == 0) {
+    int64_t Pk = 1, Sk = 1;
+    for (int j = 0; j < k; ++j) Pk *= P.dims[j];
+    for (int j = k + 1; j < P.d; ++j) Sk *= P.dims[j];
+    v.base = A;
+    if (Pk == 1) {  // column-major n_k x m
+      v.P = 1; v.S = Sk; v.sp = 1; v.si = 1; v.ss = P.dims[k];
+    } else {
+      v.P = Pk; v.S = Sk; v.sp = 1; v.si = Pk; v.ss = Pk * P.dims[k];
+    }
+  } else {
+    v.base = buf;
+    v.P = 1; v.S = mode_cols(P, k); v.sp = 1; v.si = 1; v.ss = pad4(P.dims[k]);
+  }
+  return v;
+}
+
+// Shrink of mode k reads the (k)-unfolding stored contiguously (k == 0: A itself).
+View shrink_view(const Problem& P, int k, const float* A, const float* buf) {
+  View v;
+  v.n = (int)P.dims[k];
+  v.P = 1;
+  int64_t m = 1;
+  for (int j = 0; j < P.d; ++j)
+    if (j != k) m *= (j < k) ? P.ranks[j] : P.dims[j];
+  v.S = m;
+  v.sp = 1; v.si = 1;
+  if (k == 0) { v.base = A; v.ss = P.dims[0]; }
+  else { v.base = buf; v.ss = pad4(P.dims[k]); }
+  return v;
+}
+
+struct Layout {
+  size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
+  size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
+  size_t shr_elems = 0;
+  std::vector<TilePlan> sk, pw, sh;
+};
+
+Layout plan(const Problem& P, int nsm) {
+  Layout L;
+  size_t ypart = 0, nl = 0, qsz = 0, gp = 0, ll = 0, lmax = 0;
+  L.sk.resize(P.d); L.pw.resize(P.d); L.sh.resize(P.d);
+  size_t shr = 0;
+  for (int k = 0; k < P.d; ++k) {
+    const int l = P.ranks[k] + P.p;
+    View rv = range_view(P, k, nullptr, nullptr);
+    L.sk[k] = plan_tile(rv, l, OP_SKETCH, nsm);
+    L.pw[k] = plan_tile(rv, l, OP_POWER, nsm);
+    View sv = shrink_view(P, k, nullptr, nullptr);
+    L.sh[k] = plan_tile(sv, P.ranks[k], OP_SHRINK, nsm);
+    for (const TilePlan* tp : {&L.sk[k], &L.pw[k]})
+      ypart = std::max(ypart, (size_t)tp->G * tp->ltot() * tp->n_rows());
+    const size_t n = (size_t)P.dims[k];
+    nl = std::max(nl, n * l);
+    qsz = std::max(qsz, n * l);
+    gp = std::max(gp, (size_t)((n + kRB - 1) / kRB) * l * l);
+    ll = std::max(ll, (size_t)l * l);
+    lmax = std::max(lmax, (size_t)l);
+    if (k + 1 < P.d) {
+      // output of shrink k: (r_1..r_k) x pad4(n_{k+1}) x (n_{k+2}..n_d)
+      size_t e = (size_t)pad4(P.dims[k + 1]);
+      for (int j = 0; j <= k; ++j) e *= P.ranks[j];
+      for (int j = k + 2; j < P.d; ++j) e *= P.dims[j];
+      shr = std::max(shr, e);
+    }
+  }
+  L.shr_elems = shr;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off += align_up(std::max<size_t>(bytes, 16)); return o; };
+  L.ypart = take(ypart * 4);
+  L.y = take(nl * 8);
+  L.q1 = take(nl * 8);
+  L.qd = take(nl * 8);
+  L.qs = take(qsz * 4);
+  L.gpart = take(gp * 8);
+  L.T = take(ll * 8);
+  L.lam = take(lmax * 8);
+  L.alpha = take(P.d * 8);
+  L.trace = take((size_t)P.d * P.q * 8);
+  L.sigma = take((size_t)P.d * 128 * 8);
+  L.status = take((size_t)P.d * 4 * 4);
+  L.sighat = take(lmax * 8);
+  L.shr0 = take(shr * 4);
+  L.shr1 = take(shr * 4);
+  L.total = off;
+  return L;
+}
+
+#define RTK_CK(x)                                                                          \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(RTK_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Alg. 3/4 lines 3-12 for one mode (mode index k, 0-based); writes U_k.
+int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, uint64_t seed,
+             bool shift, float* Uk, cudaStream_t st) {
+  const int n = v.n, r = P.ranks[k], l = r + P.p;
+  ModeBufs B;
+  B.n = n; B.l = l; B.r = r;
+  B.Ypart = (float*)(ws + L.ypart);
+  B.Y = (double*)(ws + L.y);
+  B.Q1 = (double*)(ws + L.q1);
+  B.Qd = (double*)(ws + L.qd);
+  B.Qs = (float*)(ws + L.qs);
+  B.gpart = (double*)(ws + L.gpart);
+  B.nblk = (n + kRB - 1) / kRB;
+  B.T = (double*)(ws + L.T);
+  B.lam = (double*)(ws + L.lam);
+  B.alpha = (double*)(ws + L.alpha) + k;
+  B.trace = (double*)(ws + L.trace) + (size_t)k * P.q;
+  B.sigma = (double*)(ws + L.sigma) + (size_t)k * 128;
+  B.status = (int*)(ws + L.status) + 4 * k;
+  B.sighat = (double*)(ws + L.sighat);
+  RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
+  const uint32_t mode1 = (uint32_t)(k + 1);
+  for (int step = 0; step <= P.q; ++step) {
+    const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
+    TileLaunch T;
+    T.v = v;
+    T.op = step == 0 ? OP_SKETCH : OP_POWER;
+    T.tp = tp;
+    T.l = l;
+    T.Q = B.Qs;
+    T.qld = n;
+    T.Ypart = B.Ypart;
+    T.seed = seed;
+    T.mode = mode1;
+    RTK_CK(launch_tile(T, st));
+    B.G = tp.G; B.ltot = tp.ltot(); B.n_rows = tp.n_rows();
+    RTK_CK(launch_reduce_gram(B, step > 0, st));
+    RTK_CK(launch_eig(B, step, P.q, shift, 0.0, st));
+    RTK_CK(launch_apply(B, seed, mode1, step, st));
+    RTK_CK(launch_chol(B, st));
+    RTK_CK(launch_apply2(B, st));
+  }
+  RTK_CK(launch_final_u(B, Uk, st));
+  return RTK_OK;
+}
+
+// G x_k U_k^T written as the next unfolding (or the canonical core after mode d).
+int run_shrink(const Problem& P, const Layout& L, int k, const View& v, const float* Uk, float* out,
+               cudaStream_t st) {
+  TileLaunch T;
+  T.v = v;
+  T.op = OP_SHRINK;
+  T.tp = L.sh[k];
+  T.l = P.ranks[k];
+  T.Q = Uk;
+  T.qld = (int)P.dims[k];
+  int64_t Rprev = 1;
+  for (int j = 0; j < k; ++j) Rprev *= P.ranks[j];
+  T.Rprev = Rprev;
+  if (k + 1 < P.d) { T.nnext = P.dims[k + 1]; T.ldnext = pad4(P.dims[k + 1]); }
+  else { T.nnext = 1; T.ldnext = 1; }
+  T.out = out;
+  RTK_CK(launch_tile(T, st));
+  return RTK_OK;
+}
+
+int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+          int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws_in,
+          size_t ws_bytes, void* stream, rtk_report* rep) {
+  if (!A || !dims || !ranks || !U || !core) return fail(RTK_ERR_ARG, "NULL pointer argument");
+  if (d < 2 || d > 8) return fail(RTK_ERR_ARG, "d must be in [2, 8]");
+  Problem P;
+  P.d = d; P.p = p; P.q = q; P.seq = opt.sequential != 0;
+  P.dims.assign(dims, dims + d);
+  P.ranks.assign(ranks, ranks + d);
+  for (int k = 0; k < d; ++k)
+    if (!U[k]) return fail(RTK_ERR_ARG, "NULL U[k]");
+  int rc = validate(P);
+  if (rc) return rc;
+  if ((uintptr_t)A % 4) return fail(RTK_ERR_ALIGN, "A must be 4-byte aligned");
+  if (opt.pve_tol > 0.0) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) is not implemented on the GPU path yet");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Layout L = plan(P, num_sms());
+  char* ws = (char*)ws_in;
+  bool own = false;
+  if (!ws) {
+    RTK_CK(cudaMallocAsync((void**)&ws, L.total, st));
+    own = true;
+  } else if (ws_bytes < L.total) {
+    return fail(RTK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  }
+  RTK_CK(cudaMemsetAsync(ws + L.status, 0, (size_t)d * 4 * 4, st));
+  RTK_CK(cudaMemsetAsync(ws + L.trace, 0, (size_t)d * q * 8, st));
+  float* shr[2] = {(float*)(ws + L.shr0), (float*)(ws + L.shr1)};
+  const bool shift = opt.shift != 0;
+  if (P.seq) {
+    // Alg. 4: factor G_(k), then G = G x_k U_k^T
+    for (int k = 0; k < d; ++k) {
+      const float* cur = k == 0 ? A : shr[(k - 1) & 1];
+      const View rv = range_view(P, k, A, cur);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      if (rc) return rc;
+      const View sv = shrink_view(P, k, A, cur);
+      rc = run_shrink(P, L, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
+      if (rc) return rc;
+    }
+  } else {
+    // Alg. 3: every mode factors the original A_(k) through its strided view
+    for (int k = 0; k < d; ++k) {
+      const View rv = range_view(P, k, A, nullptr);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      if (rc) return rc;
+    }
+    // core = A x_1 U_1^T ... x_d U_d^T, same shrink chain
+    for (int k = 0; k < d; ++k) {
+      const float* cur = k == 0 ? A : shr[(k - 1) & 1];
+      const View sv = shrink_view(P, k, A, cur);
+      rc = run_shrink(P, L, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
+      if (rc) return rc;
+    }
+  }
+  if (rep) {
+    RTK_CK(cudaStreamSynchronize(st));
+    std::vector<int> status((size_t)d * 4);
+    RTK_CK(cudaMemcpy(status.data(), ws + L.status, status.size() * 4, cudaMemcpyDeviceToHost));
+    if (rep->alpha_trace)
+      RTK_CK(cudaMemcpy(rep->alpha_trace, ws + L.trace, (size_t)d * q * 8, cudaMemcpyDeviceToHost));
+    if (rep->sigma)
+      RTK_CK(cudaMemcpy(rep->sigma, ws + L.sigma, (size_t)d * 128 * 8, cudaMemcpyDeviceToHost));
+    rep->fallback = 0;
+    rep->numeric = 0;
+    for (int k = 0; k < d; ++k) {
+      if (rep->q_used) rep->q_used[k] = status[4 * k + 2];
+      rep->fallback += status[4 * k + 1];
+      if (status[4 * k]) rep->numeric = RTK_ERR_NUMERIC;
+    }
+  }
+  if (own) RTK_CK(cudaFreeAsync(ws, st));
+  RTK_CK(cudaGetLastError());
+  return RTK_OK;
+}
+
+}  // namespace
+}  // namespace rtk
+
+using namespace rtk;
+
+extern "C" {
+
+int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+              int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws,
+              size_t ws_bytes, void* stream, rtk_report* rep) {
+  rtk_options o = {1, 1, 0.0, 0};
+  if (opt) o = *opt;
+  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+}
+
+int rtk_rthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
+                int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
+                void* stream, rtk_report* rep) {
+  rtk_options o = {0, 1, 0.0, 0};
+  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+}
+
+int rtk_rsthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
+                 int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
+                 void* stream, rtk_report* rep) {
+  rtk_options o = {1, 1, 0.0, 0};
+  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+}
+
+size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
+                           int32_t q) {
+  if (!dims || !ranks || d < 2 || d > 8) {
+    g_err = "invalid arguments";
+    return 0;
+  }
+  Problem P;
+  P.d = d; P.p = p; P.q = q; P.seq = algo != 0;
+  P.dims.assign(dims, dims + d);
+  P.ranks.assign(ranks, ranks + d);
+  if (validate(P)) return 0;
+  return plan(P, num_sms()).total;
+}
+
+int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out, void* stream) {
+  if (!out || rows < 0 || row0 < 0 || l < 1 || mode < 0) return fail(RTK_ERR_ARG, "invalid rtk_omega arguments");
+  if (rows == 0) return RTK_OK;
+  cudaError_t e = launch_omega(seed, (uint32_t)mode, row0, rows, l, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(RTK_ERR_CUDA, cudaGetErrorString(e));
+  return RTK_OK;
+}
+
+int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float* Q, int32_t l, double* Y,
+                   void* stream) {
+  if (!M || !Q || !Y || n < 1 || m < 1 || ld < n || l < 1 || n > kNMax)
+    return fail(RTK_ERR_ARG, "invalid rtk_power_step arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  View v;
+  v.base = M; v.n = (int)n; v.P = 1; v.S = m; v.sp = 1; v.si = 1; v.ss = ld;
+  TileLaunch T;
+  T.v = v;
+  T.op = OP_POWER;
+  T.tp = plan_tile(v, l, OP_POWER, num_sms());
+  T.l = l;
+  T.Q = Q;
+  T.qld = (int)n;
+  float* yp = nullptr;
+  const size_t bytes = (size_t)T.tp.G * T.tp.ltot() * T.tp.n_rows() * 4;
+  RTK_CK(cudaMallocAsync((void**)&yp, bytes, st));
+  T.Ypart = yp;
+  RTK_CK(launch_tile(T, st));
+  RTK_CK(launch_sum_partials(yp, T.tp.G, T.tp.ltot(), T.tp.n_rows(), (int)n, l, Y, st));
+  RTK_CK(cudaFreeAsync(yp, st));
+  return RTK_OK;
+}
+
+const char* rtk_last_error(void) { return g_err.c_str(); }
+
+const char* rtk_version(void) { return "rtucker 0.1.0 sm_100a"; }
+
+}  // extern "C"

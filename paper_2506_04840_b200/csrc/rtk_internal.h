@@ -1,0 +1,92 @@
+// rtk_internal.h -- host-side plumbing shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+namespace rtk {
+
+// Matrix view of a mode-k unfolding M (n x m), column j = p + P*s  (p < P, s < S):
+// element (i, j) at base[p*sp + i*si + s*ss].  A column-major matrix with leading
+// dimension ld is the view P = 1, S = m, si = 1, ss = ld.
+struct View {
+  const float* base = nullptr;
+  int64_t P = 1, S = 1;
+  int64_t sp = 1, si = 1, ss = 1;
+  int n = 0;
+  int64_t m() const { return P * S; }
+};
+
+enum TileOp { OP_SKETCH = 0, OP_POWER = 1, OP_SHRINK = 2 };
+
+// Tile-kernel configuration chosen by the planner (rtk_plan.cu).
+struct TilePlan {
+  int R = 4;       // rows per thread
+  int TC = 8;      // columns per thread
+  int NRG = 0;     // row groups (n_rows = R*NRG)
+  int NCG = 1;     // column groups per chunk (power of two, divides 32)
+  int LC = 8;      // columns per chunk = NCG*TC
+  int nchunks = 1;
+  int NT = 32;     // threads per CTA (multiple of 32, >= NRG_pad*NCG)
+  int b = 16;      // tile width (columns)
+  int pitch = 0;   // SMEM column pitch (floats)
+  int G = 1;       // CTAs per chunk
+  int64_t ntiles = 0;
+  size_t smem = 0;
+  int n_rows() const { return R * NRG; }
+  int ltot() const { return nchunks * LC; }
+};
+
+struct TileLaunch {
+  View v;
+  TileOp op;
+  TilePlan tp;
+  int l = 0;                  // valid columns (sketch l or shrink r)
+  const float* Q = nullptr;   // POWER: fp32 Q [c][i] (ld qld); SHRINK: U n x r col-major (ld qld)
+  int qld = 0;
+  float* Ypart = nullptr;     // [G][ltot][n_rows]
+  uint64_t seed = 0;
+  uint32_t mode = 0;
+  float* out = nullptr;       // SHRINK destination
+  int64_t Rprev = 1, nnext = 1, ldnext = 1;
+};
+
+TilePlan plan_tile(const View& v, int l, TileOp op, int num_sms);
+cudaError_t launch_tile(const TileLaunch& L, cudaStream_t st);
+
+// ---- small-solve kernels (rtk_small.cu) -------------------------------------
+struct ModeBufs {
+  int n = 0, l = 0, r = 0, G = 1, ltot = 0, n_rows = 0;
+  float* Ypart = nullptr;   // [G][ltot][n_rows]
+  double* Y = nullptr;      // [l][n]
+  double* Q1 = nullptr;     // [l][n]
+  double* Qd = nullptr;     // [l][n]  fp64 master basis
+  float* Qs = nullptr;      // [l][n]  fp32 shadow for the stream
+  double* gpart = nullptr;  // [nblk][l][l]
+  int nblk = 0;
+  double* T = nullptr;      // [l][l] (column-major)
+  double* lam = nullptr;    // [l]
+  double* alpha = nullptr;  // device scalar for this mode
+  double* trace = nullptr;  // [q] alpha trace
+  double* sigma = nullptr;  // [128] final sigma estimates
+  int* status = nullptr;    // [0]=numeric, [1]=fallback count, [2]=q_used, [3]=pve_stop
+  double* sighat = nullptr; // [l] B.1 sigma-hat
+};
+
+cudaError_t launch_reduce_gram(const ModeBufs& B, bool power, cudaStream_t st);
+cudaError_t launch_eig(const ModeBufs& B, int step, int q, bool shift, double pve_tol,
+                       cudaStream_t st);
+cudaError_t launch_apply(const ModeBufs& B, uint64_t seed, uint32_t mode, int step,
+                         cudaStream_t st);
+cudaError_t launch_chol(const ModeBufs& B, cudaStream_t st);
+cudaError_t launch_apply2(const ModeBufs& B, cudaStream_t st);
+cudaError_t launch_final_u(const ModeBufs& B, float* U, cudaStream_t st);
+cudaError_t launch_omega(uint64_t seed, uint32_t mode, int64_t row0, int64_t rows, int l,
+                         float* out, cudaStream_t st);
+cudaError_t launch_sum_partials(const float* Ypart, int G, int ltot, int n_rows, int n, int l,
+                                double* Y, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace rtk

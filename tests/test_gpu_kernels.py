@@ -1,0 +1,72 @@
+"""GPU kernels in isolation vs the oracle / fp64 brute force (through the C ABI)."""
+import numpy as np
+import pytest
+
+from oracle import gauss
+from workloads import CONFIGS
+from tests.gpu_util import cuda_or_skip
+
+pytestmark = pytest.mark.gpu
+
+
+def test_omega_bit_exact_small():
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import omega
+    for seed, mode, row0, rows, l in [(1, 1, 0, 1000, 16), (1234567890123, 3, 5, 777, 15),
+                                      (2**63 + 11, 8, 2**32 - 3, 9, 7), (0, 0, 0, 4, 1)]:
+        g = omega(seed, mode, row0, rows, l).cpu().numpy()
+        o = gauss.omega(seed, mode, row0, rows, l)
+        np.testing.assert_array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", list(CONFIGS))
+def test_omega_bit_exact_config_shapes(cfg):
+    """Every (mode, m_k, l_k) the five configs draw: first, last and random rows."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import omega
+    c = CONFIGS[cfg]
+    dims, ranks, p = c["dims"], c["ranks"], c["p"]
+    rng = np.random.default_rng(0)
+    for k in range(len(dims)):
+        m = 1
+        for j in range(len(dims)):
+            if j != k:
+                m *= ranks[j] if (c["algo"] == "rsthosvd" and j < k) else dims[j]
+        l = ranks[k] + p
+        starts = sorted(set([0, max(0, m - 512)] + list(rng.integers(0, max(1, m - 512), 4))))
+        for r0 in starts:
+            rows = min(512, m - r0)
+            g = omega(c["omega_seed"], k + 1, int(r0), rows, l).cpu().numpy()
+            o = gauss.omega(c["omega_seed"], k + 1, int(r0), rows, l)
+            np.testing.assert_array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+@pytest.mark.parametrize("n,m,l", [(1, 7, 1), (3, 50, 2), (64, 4096, 10), (80, 1000, 15),
+                                   (200, 3000, 30), (400, 2001, 40), (1000, 1234, 60),
+                                   (37, 333, 13), (1500, 700, 20), (4096, 100, 8), (130, 5000, 64)])
+def test_power_step_vs_fp64(n, m, l):
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import power_step
+    rng = np.random.default_rng(n * 7 + m)
+    M = rng.standard_normal((n, m)).astype(np.float32)
+    Q = np.linalg.qr(rng.standard_normal((n, l)))[0].astype(np.float32)
+    Md = torch.from_numpy(np.asfortranarray(M)).cuda()
+    Y = power_step(Md, torch.from_numpy(Q).cuda()).cpu().numpy()
+    ref = M.astype(np.float64) @ (M.astype(np.float64).T @ Q.astype(np.float64))
+    err = np.linalg.norm(Y - ref) / np.linalg.norm(ref)
+    assert err < 2e-6, err
+
+
+def test_power_step_padded_leading_dimension():
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import power_step
+    rng = np.random.default_rng(5)
+    n, m, l, ld = 102, 999, 12, 104
+    buf = np.zeros((ld, m), dtype=np.float32, order="F")
+    buf[:n] = rng.standard_normal((n, m))
+    Q = rng.standard_normal((n, l)).astype(np.float32)
+    Md = torch.from_numpy(buf).cuda()[:n]
+    Y = power_step(Md, torch.from_numpy(Q).cuda()).cpu().numpy()
+    M = buf[:n].astype(np.float64)
+    ref = M @ (M.T @ Q.astype(np.float64))
+    assert np.linalg.norm(Y - ref) / np.linalg.norm(ref) < 2e-6
