@@ -123,6 +123,21 @@ RTK_API int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, i
 RTK_API int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float* Q, int32_t l,
                    double* Y, void* stream);
 
+/* Device-time profile of the library's own launches (bench / roofline evidence).
+ * Between rtk_profile_begin() and rtk_profile_end() every streaming-kernel launch
+ * (and every per-step small-solve sequence) is bracketed by CUDA events on the
+ * launching stream; rtk_profile_end() synchronises those events and reports the
+ * summed milliseconds and counts by (kind, mode), plus the number of kernels the
+ * library launched.  kind: 0 sketch tile, 1 power-step tile, 2 shrink tile,
+ * 3 small solves (reduce..apply2 of one step).  mode: 0-based, < 8. */
+typedef struct rtk_prof_stats {
+  double ms[4][8];
+  int32_t count[4][8];
+  int64_t launches;
+} rtk_prof_stats;
+RTK_API int rtk_profile_begin(void);
+RTK_API int rtk_profile_end(rtk_prof_stats* out);
+
 /* Thread-local message for the last non-zero status. */
 RTK_API const char* rtk_last_error(void);
 

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_omega",
-                 "rtk_power_step", "rtk_last_error", "rtk_version"]
+                 "rtk_power_step", "rtk_profile_begin", "rtk_profile_end", "rtk_last_error",
+                 "rtk_version"]
 
 RTK_STATUS = {0: "RTK_OK", 1: "RTK_ERR_ARG", 2: "RTK_ERR_SHAPE", 3: "RTK_ERR_ALIGN",
               4: "RTK_ERR_WORKSPACE", 5: "RTK_ERR_CUDA", 6: "RTK_ERR_NUMERIC"}
@@ -27,6 +28,11 @@ class _Report(ctypes.Structure):
                 ("q_used", ctypes.POINTER(ctypes.c_int32)),
                 ("fallback", ctypes.c_int32),
                 ("numeric", ctypes.c_int32)]
+
+
+class ProfStats(ctypes.Structure):
+    _fields_ = [("ms", (ctypes.c_double * 8) * 4), ("count", (ctypes.c_int32 * 8) * 4),
+                ("launches", ctypes.c_int64)]
 
 
 class _Options(ctypes.Structure):
@@ -68,10 +74,26 @@ def load_library():
     lib.rtk_power_step.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, vp,
                                    ctypes.c_int32, vp, vp]
     lib.rtk_power_step.restype = ctypes.c_int
+    lib.rtk_profile_begin.argtypes = []
+    lib.rtk_profile_begin.restype = ctypes.c_int
+    lib.rtk_profile_end.argtypes = [ctypes.POINTER(ProfStats)]
+    lib.rtk_profile_end.restype = ctypes.c_int
     lib.rtk_last_error.restype = ctypes.c_char_p
     lib.rtk_version.restype = ctypes.c_char_p
     _LIB = lib
     return lib
+
+
+def profile_begin():
+    """Start recording CUDA events around the library's launches (see rtk_profile_begin)."""
+    _check(load_library().rtk_profile_begin())
+
+
+def profile_end() -> ProfStats:
+    """Stop recording; returns summed device ms / counts by (kind, mode) and #launches."""
+    st = ProfStats()
+    _check(load_library().rtk_profile_end(ctypes.byref(st)))
+    return st
 
 
 def version() -> str:
@@ -230,9 +252,9 @@ def power_step(M, Q):
     import torch
     lib = load_library()
     n, m = M.shape
-    if M.stride(0) != 1 or M.dtype != torch.float32 or not M.is_cuda:
+    if (M.stride(0) != 1 and n > 1) or M.dtype != torch.float32 or not M.is_cuda:
         raise ValueError("M must be a column-major float32 CUDA matrix")
-    ld = M.stride(1) if m > 1 else n
+    ld = max(M.stride(1), n) if m > 1 else n
     l = Q.shape[1]
     Qc = Q.t().contiguous()                     # column-major n x l, ld n
     Y = torch.empty((l, n), dtype=torch.float64, device=M.device)

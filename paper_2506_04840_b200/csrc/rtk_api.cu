@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +21,36 @@ namespace rtk {
 namespace {
 
 thread_local std::string g_err;
+
+// ---- launch accounting / optional event profile (rtk_profile_begin/end) ----
+struct ProfRec {
+  int kind, mode;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::atomic<bool> g_prof_on{false};
+std::atomic<long long> g_launches{0};
+
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int kind, mode;
+  cudaStream_t st;
+  ProfScope(int kind_, int mode_, cudaStream_t st_) : kind(kind_), mode(mode_), st(st_) {
+    if (g_prof_on.load()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof.push_back({kind, mode, a, b});
+    }
+  }
+};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -204,15 +236,23 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     T.Ypart = B.Ypart;
     T.seed = seed;
     T.mode = mode1;
-    RTK_CK(launch_tile(T, st));
+    {
+      ProfScope ps(step == 0 ? 0 : 1, k, st);
+      RTK_CK(launch_tile(T, st));
+    }
     B.G = tp.G; B.ltot = tp.ltot(); B.n_rows = tp.n_rows();
-    RTK_CK(launch_reduce_gram(B, step > 0, st));
-    RTK_CK(launch_eig(B, step, P.q, shift, 0.0, st));
-    RTK_CK(launch_apply(B, seed, mode1, step, st));
-    RTK_CK(launch_chol(B, st));
-    RTK_CK(launch_apply2(B, st));
+    {
+      ProfScope ps(3, k, st);
+      RTK_CK(launch_reduce_gram(B, step > 0, st));
+      RTK_CK(launch_eig(B, step, P.q, shift, 0.0, st));
+      RTK_CK(launch_apply(B, seed, mode1, step, st));
+      RTK_CK(launch_chol(B, st));
+      RTK_CK(launch_apply2(B, st));
+    }
+    g_launches += 6;
   }
   RTK_CK(launch_final_u(B, Uk, st));
+  g_launches += 1;
   return RTK_OK;
 }
 
@@ -232,7 +272,9 @@ int run_shrink(const Problem& P, const Layout& L, int k, const View& v, const fl
   if (k + 1 < P.d) { T.nnext = P.dims[k + 1]; T.ldnext = pad4(P.dims[k + 1]); }
   else { T.nnext = 1; T.ldnext = 1; }
   T.out = out;
+  ProfScope ps(2, k, st);
   RTK_CK(launch_tile(T, st));
+  g_launches += 1;
   return RTK_OK;
 }
 
@@ -385,6 +427,40 @@ int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float
   RTK_CK(launch_sum_partials(yp, T.tp.G, T.tp.ltot(), T.tp.n_rows(), (int)n, l, Y, st));
   RTK_CK(cudaFreeAsync(yp, st));
   return RTK_OK;
+}
+
+int rtk_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  g_launches = 0;
+  g_prof_on = true;
+  return RTK_OK;
+}
+
+int rtk_profile_end(rtk_prof_stats* out) {
+  g_prof_on = false;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (out) std::memset(out, 0, sizeof(*out));
+  int rc = RTK_OK;
+  for (auto& r : g_prof) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess) rc = fail(RTK_ERR_CUDA, cudaGetErrorString(e));
+    if (out && r.kind >= 0 && r.kind < 4 && r.mode >= 0 && r.mode < 8) {
+      out->ms[r.kind][r.mode] += ms;
+      out->count[r.kind][r.mode] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  if (out) out->launches = g_launches.load();
+  return rc;
 }
 
 const char* rtk_last_error(void) { return g_err.c_str(); }

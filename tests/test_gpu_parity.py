@@ -59,7 +59,7 @@ def test_config_parity(cfg):
 
 @pytest.mark.parametrize("seq", [False, True])
 @pytest.mark.parametrize("dims,ranks,p,q", [
-    ((40, 30), (5, 4), 3, 2),                 # d = 2, the matrix case
+    ((40, 30), (6, 4), 2, 2),                 # d = 2, the matrix case
     ((37, 29, 23), (4, 5, 3), 3, 2),          # odd sizes: scalar loader, ragged tiles
     ((16, 12, 10, 9), (3, 2, 4, 2), 2, 3),    # d = 4
     ((260, 18, 15), (6, 5, 4), 4, 2),         # n_1 > 256 (multi-row threads)
