@@ -163,7 +163,7 @@ Layout plan(const Problem& P, int nsm) {
     const size_t n = (size_t)P.dims[k];
     nl = std::max(nl, n * l);
     qsz = std::max(qsz, n * l);
-    gp = std::max(gp, (size_t)((n + kRB - 1) / kRB) * l * l);
+    gp = std::max(gp, (size_t)((n + 63) / 64) * l * (l + 1) / 2);
     ll = std::max(ll, (size_t)l * l);
     lmax = std::max(lmax, (size_t)l);
     if (k + 1 < P.d) {
@@ -214,7 +214,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   B.Qd = (double*)(ws + L.qd);
   B.Qs = (float*)(ws + L.qs);
   B.gpart = (double*)(ws + L.gpart);
-  B.nblk = (n + kRB - 1) / kRB;
+  B.nblk = (n + 63) / 64;   // kGB-row Gram blocks (rtk_small.cu)
   B.T = (double*)(ws + L.T);
   B.lam = (double*)(ws + L.lam);
   B.alpha = (double*)(ws + L.alpha) + k;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "rtk_gauss.cuh"
 #include "rtk_internal.h"
@@ -117,7 +118,7 @@ __device__ __forceinline__ void issue_tile(const TileArgs& a, int64_t t, float* 
   }
 }
 
-template <int R, int TC, int OP>
+template <int R, int TC, int OP, int U = 4>
 __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
   extern __shared__ __align__(16) float smem[];
   float* Mbuf0 = smem;
@@ -183,50 +184,57 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
     __syncthreads();
 
     if constexpr (OP != OP_SKETCH) {
-      // ---- step A: partial W over this thread's rows, reduced across the warp ----
-      for (int j = 0; j < a.b; ++j) {
-        float mv[R];
-        if (active) load_col<R>(Ms + j * a.pitch, rg, a.NRG, mv);
-        else {
+      // ---- step A: partial W over this thread's rows for U columns at a time, then
+      // one batched transpose-reduce across the lanes sharing cg (lane bits >= log2 NCG).
+      constexpr int NV = U * TC;
+      const int nsteps = 5 - (31 - __clz(a.NCG));
+      const int cnt = (nsteps >= 31 - __clz(NV)) ? 1 : (NV >> nsteps);
+      for (int j0 = 0; j0 < a.b; j0 += U) {
+        float mv[U][R];
 #pragma unroll
-          for (int e = 0; e < R; ++e) mv[e] = 0.f;
+        for (int u = 0; u < U; ++u) {
+          if (active) load_col<R>(Ms + (j0 + u) * a.pitch, rg, a.NRG, mv[u]);
+          else {
+#pragma unroll
+            for (int e = 0; e < R; ++e) mv[u][e] = 0.f;
+          }
         }
-        float v[TC];
+        float v[NV];
 #pragma unroll
-        for (int c = 0; c < TC; ++c) {
-          float s = 0.f;
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int e = 0; e < R; ++e) s = fmaf(mv[e], qv[e][c], s);
-          v[c] = s;
-        }
-        // transpose-reduce over the lanes sharing cg (lane bits >= log2(NCG)):
-        // step s uses lane mask 16>>s and halves the live values while more than one
-        // remains (compile-time indices; only the step count is runtime).
+          for (int c = 0; c < TC; ++c) {
+            float s = 0.f;
+#pragma unroll
+            for (int e = 0; e < R; ++e) s = fmaf(mv[u][e], qv[e][c], s);
+            v[u * TC + c] = s;
+          }
         int coff = 0;
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
           const int mask = 16 >> s;
           if (mask >= a.NCG) {
-            if ((TC >> s) >= 2) {
+            if ((NV >> s) >= 2) {
               const bool up = (lane & mask) != 0;
 #pragma unroll
-              for (int i = 0; i < (TC >> (s + 1)); ++i) {
-                const float send = up ? v[i] : v[i + (TC >> (s + 1))];
-                const float keep = up ? v[i + (TC >> (s + 1))] : v[i];
+              for (int i = 0; i < (NV >> (s + 1)); ++i) {
+                const float send = up ? v[i] : v[i + (NV >> (s + 1))];
+                const float keep = up ? v[i + (NV >> (s + 1))] : v[i];
                 v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
               }
-              if (up) coff += TC >> (s + 1);
+              if (up) coff += NV >> (s + 1);
             } else {
               v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
             }
           }
         }
-        const int nsteps = 5 - (31 - __clz(a.NCG));
-        const int cnt = (nsteps >= 31 - __clz(TC)) ? 1 : (TC >> nsteps);
-        float* rw = red + ((size_t)warp * a.b + j) * a.LC + cg * TC + coff;
+        float* rw = red + ((size_t)warp * a.b + j0) * a.LC + cg * TC;
 #pragma unroll
-        for (int i = 0; i < TC; ++i)
-          if (i < cnt) rw[i] = v[i];
+        for (int i = 0; i < NV; ++i)
+          if (i < cnt) {
+            const int f = coff + i;
+            rw[(f / TC) * a.LC + (f % TC)] = v[i];
+          }
       }
       __syncthreads();
       // ---- cross-warp sum in fixed order -> W ----
@@ -258,22 +266,27 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
         }
       }
     } else {
-      // ---- step B: Y += M_J W_J on this thread's rows x TC columns ----
+      // ---- step B: Y += M_J W_J on this thread's rows x TC columns, U columns at a time ----
       if (active) {
         const float* wrow = Wsm + cg * TC;
-        for (int j = 0; j < a.b; ++j) {
-          float mv[R];
-          load_col<R>(Ms + j * a.pitch, rg, a.NRG, mv);
-          float wv[TC];
+        for (int j0 = 0; j0 < a.b; j0 += U) {
+          float mv[U][R];
+          float wv[U][TC];
 #pragma unroll
-          for (int c = 0; c < TC; c += 4) {
-            const float4 w4 = *reinterpret_cast<const float4*>(wrow + j * a.LC + c);
-            wv[c] = w4.x; wv[c + 1] = w4.y; wv[c + 2] = w4.z; wv[c + 3] = w4.w;
+          for (int u = 0; u < U; ++u) {
+            load_col<R>(Ms + (j0 + u) * a.pitch, rg, a.NRG, mv[u]);
+#pragma unroll
+            for (int c = 0; c < TC; c += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wrow + (j0 + u) * a.LC + c);
+              wv[u][c] = w4.x; wv[u][c + 1] = w4.y; wv[u][c + 2] = w4.z; wv[u][c + 3] = w4.w;
+            }
           }
 #pragma unroll
-          for (int e = 0; e < R; ++e)
+          for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int c = 0; c < TC; ++c) acc[e][c] = fmaf(mv[e], wv[c], acc[e][c]);
+            for (int e = 0; e < R; ++e)
+#pragma unroll
+              for (int c = 0; c < TC; ++c) acc[e][c] = fmaf(mv[u][e], wv[u][c], acc[e][c]);
         }
       }
     }
@@ -371,8 +384,30 @@ TilePlan plan_tile(const View& v, int l, TileOp op, int nsm) {
       }
     }
   }
+  // tuning override: RTK_PLAN_<op>="R,TC,NCG,b" (op = SKETCH|POWER|SHRINK) or RTK_PLAN
+  const char* names[3] = {"RTK_PLAN_SKETCH", "RTK_PLAN_POWER", "RTK_PLAN_SHRINK"};
+  const char* ov = getenv(names[op]);
+  if (!ov) ov = getenv("RTK_PLAN");
+  int oR, oTC, oNCG, ob;
+  if (ov && sscanf(ov, "%d,%d,%d,%d", &oR, &oTC, &oNCG, &ob) == 4) {
+    const int NRG = (n + oR - 1) / oR;
+    const int lanes = 32 / oNCG;
+    const int NRGp = (NRG + lanes - 1) / lanes * lanes;
+    best.R = oR; best.TC = oTC; best.NCG = oNCG; best.NRG = NRG; best.LC = oNCG * oTC;
+    best.nchunks = (l + best.LC - 1) / best.LC; best.NT = NRGp * oNCG; best.b = ob;
+    best.pitch = (oR * NRG + 3) / 4 * 4;
+    best.smem = tile_smem(ob, best.pitch, best.LC, best.NT);
+    const int regs = 2 * oR * oTC + 40;
+    const int occ = std::max(1, std::min<int>(std::max(1, 65536 / (best.NT * regs)),
+                                              (int)((228 * 1024) / (best.smem + 1024))));
+    best.G = std::max(1, nsm * occ / best.nchunks);
+  }
   best.ntiles = (v.m() + best.b - 1) / best.b;
   if (best.G > best.ntiles) best.G = (int)best.ntiles;
+  if (getenv("RTK_VERBOSE"))
+    fprintf(stderr, "[rtk] plan op=%d n=%d m=%lld l=%d: R=%d TC=%d NCG=%d LC=%d chunks=%d NT=%d b=%d G=%d smem=%zu\n",
+            (int)op, n, (long long)v.m(), l, best.R, best.TC, best.NCG, best.LC, best.nchunks, best.NT,
+            best.b, best.G, best.smem);
   return best;
 }
 
