@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(512) eig_kernel(const double* __restrict__ gpa
   __syncthreads();
 
   for (int sweep = 0; sweep < 40; ++sweep) {
+    __syncthreads();                 // everyone has read any_rot of the previous sweep
     if (tid == 0) any_rot = 0;
     for (int rnd = 0; rnd < le - 1; ++rnd) {
       __syncthreads();
@@ -296,7 +297,8 @@ __global__ void __launch_bounds__(512) eig_kernel(const double* __restrict__ gpa
       }
     }
     __syncthreads();
-    if (!any_rot) break;
+    const int rotated = any_rot;
+    if (!rotated) break;
   }
   __syncthreads();
   // sort eigenvalues descending (ties: lower index first)

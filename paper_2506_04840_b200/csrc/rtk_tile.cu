@@ -3,7 +3,7 @@
 // One templated kernel streams the mode-k unfolding M (n x m) ONCE, column
 // block by column block, and per block J (b columns) computes
 //
-//   OP_SKETCH : W_J = Omega_k(J, :)                     (RTK-GAUSS-1, in registers/SMEM)
+//   OP_SKETCH : W_J = Omega_k(J, :)                     (RTK-GAUSS-1, generated in SMEM)
 //               Y  += M_J W_J                           Alg. 3/4 line 5
 //   OP_POWER  : W_J = M_J^T Q                           Alg. 3/4 line 7
 //               Y  += M_J W_J                           -- fused single pass, M read once
@@ -13,11 +13,16 @@
 // Each CTA owns LC columns of Q/Y (a "chunk"; Y = M M^T Q is column-separable)
 // and a strided set of column blocks; Y partials are written per CTA and
 // reduced in a fixed order by rtk_small.cu (run-to-run deterministic, no float
-// atomics).  Tiles are double-buffered in shared memory with cp.async; the
-// thread-level register tiles are R rows x TC columns of Q (step A) and of Y
-// (step B).  -alpha Q is applied in the reduction epilogue.
-#include <cuda_pipeline.h>
-
+// atomics).  -alpha Q is applied in that reduction.
+//
+// Data movement: tiles are double-buffered in shared memory.  Column-major
+// unfoldings (mode 1 and every ST-HOSVD mode, whose shrink writes the next
+// unfolding contiguously) are loaded with TMA bulk copies (cp.async.bulk, one
+// elected thread, mbarrier complete_tx); strided T-HOSVD views (P > 1) use a
+// cp.async gather.  Thread work: thread (rg, cg) owns R rows x TC columns of Q
+// (registers, step A) and of Y (registers, step B); warps are (32/NCG row groups)
+// x NCG column groups, so the step-A row reduction is an in-warp transpose-reduce
+// over the lane bits >= log2(NCG) plus a fixed-order cross-warp sum.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -30,8 +35,8 @@ namespace rtk {
 struct TileArgs {
   const float* M;
   int64_t P, S, sp, si, ss, m;
-  int n, vec, n4;
-  int n_rows, pitch, NRG, NCG, LC, nchunks, G, b;
+  int n, bulk, n4;
+  int n_rows, pitch, NRG, LC, nchunks, G, b;
   int64_t ntiles;
   int l;
   const float* Q;
@@ -44,22 +49,22 @@ struct TileArgs {
   int64_t Rprev, nnext, ldnext;
 };
 
-// row held by thread row-group rg, element e (0 <= e < R)
+// row held by thread row-group rg (0 <= rg < NRGp), element e (0 <= e < R)
 template <int R>
-__device__ __forceinline__ int row_of(int rg, int e, int NRG) {
+__device__ __forceinline__ int row_of(int rg, int e, int NRGp) {
   if constexpr (R >= 4) {
-    return 4 * (rg + (e >> 2) * NRG) + (e & 3);
+    return 4 * (rg + (e >> 2) * NRGp) + (e & 3);
   } else {
     return rg * R + e;
   }
 }
 
 template <int R>
-__device__ __forceinline__ void load_col(const float* __restrict__ col, int rg, int NRG, float (&m)[R]) {
+__device__ __forceinline__ void load_col(const float* __restrict__ col, int rg, int NRGp, float (&m)[R]) {
   if constexpr (R >= 4) {
 #pragma unroll
     for (int k = 0; k < R / 4; ++k) {
-      const float4 v = *reinterpret_cast<const float4*>(col + 4 * (rg + k * NRG));
+      const float4 v = *reinterpret_cast<const float4*>(col + 4 * (rg + k * NRGp));
       m[4 * k + 0] = v.x; m[4 * k + 1] = v.y; m[4 * k + 2] = v.z; m[4 * k + 3] = v.w;
     }
   } else if constexpr (R == 2) {
@@ -70,35 +75,60 @@ __device__ __forceinline__ void load_col(const float* __restrict__ col, int rg, 
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
+// ---- async-copy primitives -----------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Issue the asynchronous copy of tile `t` (columns [t*b, t*b+b)) into Ms (pitch floats per column).
-__device__ __forceinline__ void issue_tile(const TileArgs& a, int64_t t, float* Ms) {
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Issue tile `t` (columns [t*b, t*b+b)) into Ms.
+//  bulk path : one elected thread posts expect_tx and the TMA bulk copies (one per column,
+//              or a single copy when the tile is contiguous); tail columns of a ragged last
+//              tile are zero-filled by all threads.
+//  gather    : every thread issues 4-byte cp.async (zero-filled outside the matrix).
+__device__ __forceinline__ void issue_tile(const TileArgs& a, int64_t t, float* Ms, uint64_t* bar) {
   const int64_t j0 = t * a.b;
-  if (a.vec) {
-    const int per_col = a.pitch >> 2;
-    const int total = a.b * per_col;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-      const int jj = idx / per_col;
-      const int i = (idx - jj * per_col) << 2;
-      const int64_t jg = j0 + jj;
-      int bytes = 0;
-      const float* src = a.M;
-      if (jg < a.m && i < a.n4) {
-        bytes = 16;
-        src = a.M + jg * a.ss + i;
+  const int64_t rem = a.m - j0;
+  const int jc = rem < (int64_t)a.b ? (int)rem : a.b;
+  if (a.bulk) {
+    if (jc < a.b) {
+      for (int idx = threadIdx.x; idx < (a.b - jc) * a.pitch; idx += blockDim.x) Ms[jc * a.pitch + idx] = 0.f;
+    }
+    if (threadIdx.x == 0) {
+      const unsigned colb = (unsigned)a.n4 * 4u;
+      mbar_expect_tx(bar, colb * (unsigned)jc);
+      if (a.ss == a.pitch && a.n4 == a.pitch) {
+        bulk_g2s(Ms, a.M + j0 * a.ss, colb * (unsigned)jc, bar);
+      } else {
+        for (int jj = 0; jj < jc; ++jj) bulk_g2s(Ms + jj * a.pitch, a.M + (j0 + jj) * a.ss, colb, bar);
       }
-      cp_async16(Ms + jj * a.pitch + i, src, bytes);
     }
   } else {
     const int total = a.b * a.pitch;
@@ -115,15 +145,25 @@ __device__ __forceinline__ void issue_tile(const TileArgs& a, int64_t t, float* 
       }
       cp_async4(Ms + jj * a.pitch + i, src, bytes);
     }
+    cp_async_commit();
   }
 }
 
-template <int R, int TC, int OP, int U = 4>
+template <int R, int TC, int NCG, int OP>
 __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
-  extern __shared__ __align__(16) float smem[];
+  constexpr int U = 4;                 // columns per inner batch (ILP)
+  constexpr int LOG_NCG = NCG == 1 ? 0 : NCG == 2 ? 1 : NCG == 4 ? 2 : 3;
+  constexpr int NSTEPS = 5 - LOG_NCG;  // lane bits that index row groups
+  constexpr int NV = U * TC;
+  constexpr int LOG_NV = NV >= 32 ? 5 : NV >= 16 ? 4 : NV >= 8 ? 3 : 2;
+  constexpr int CNT = NSTEPS >= LOG_NV ? 1 : (NV >> NSTEPS);
+
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const int pitch = a.pitch;
   float* Mbuf0 = smem;
-  float* Mbuf1 = smem + a.b * a.pitch;
-  float* Wsm = Mbuf1 + a.b * a.pitch;            // [b][LC]
+  float* Mbuf1 = smem + a.b * pitch;
+  float* Wsm = Mbuf1 + a.b * pitch;              // [b][LC]
   float* red = Wsm + a.b * a.LC;                 // [NW][b][LC]
 
   const int tid = threadIdx.x;
@@ -131,17 +171,32 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
   const int nwarps = blockDim.x >> 5;
   const int chunk = blockIdx.x % a.nchunks;
   const int grp = blockIdx.x / a.nchunks;
-  const int cg = tid % a.NCG;
-  const int rg = tid / a.NCG;
-  const bool active = rg < a.NRG;
+  const int cg = tid % NCG;
+  const int rg = tid / NCG;                      // < NRGp (padded row groups; rows >= n are zero)
+  const int NRGp = a.NRG;
   const int c_base = chunk * a.LC + cg * TC;     // first global column of this thread
+
+  // zero the rows [n4, pitch) of both buffers once (never written by the copies)
+  if (a.bulk) {
+    const int w = pitch - a.n4;
+    for (int idx = tid; idx < 2 * a.b * w; idx += blockDim.x) {
+      const int col = idx / w, r = a.n4 + idx % w;
+      smem[col * pitch + r] = 0.f;
+    }
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+  }
+  __syncthreads();
 
   // Q / U register tile (rows x TC), constant for the whole kernel
   float qv[R][TC];
   if constexpr (OP != OP_SKETCH) {
 #pragma unroll
     for (int e = 0; e < R; ++e) {
-      const int row = active ? row_of<R>(rg, e, a.NRG) : a.n;
+      const int row = row_of<R>(rg, e, NRGp);
 #pragma unroll
       for (int c = 0; c < TC; ++c) {
         const int col = c_base + c;
@@ -156,14 +211,15 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
     for (int c = 0; c < TC; ++c) acc[e][c] = 0.f;
 
   int64_t t = grp;
-  if (t < a.ntiles) issue_tile(a, t, Mbuf0);
-  cp_async_commit();
+  if (t < a.ntiles) issue_tile(a, t, Mbuf0, &bars[0]);
+  else if (!a.bulk) cp_async_commit();
   int buf = 0;
+  unsigned ph0 = 0, ph1 = 0;
   for (; t < a.ntiles; t += a.G) {
     float* Ms = buf ? Mbuf1 : Mbuf0;
     const int64_t tn = t + a.G;
-    if (tn < a.ntiles) issue_tile(a, tn, buf ? Mbuf0 : Mbuf1);
-    cp_async_commit();
+    if (tn < a.ntiles) issue_tile(a, tn, buf ? Mbuf0 : Mbuf1, &bars[buf ^ 1]);
+    else if (!a.bulk) cp_async_commit();
     const int64_t j0 = t * a.b;
 
     if constexpr (OP == OP_SKETCH) {
@@ -180,25 +236,21 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
         Wsm[j * a.LC + c2 + 1] = (cgl + 1 < a.l) ? z.y : 0.f;
       }
     }
-    cp_async_wait<1>();
+    if (a.bulk) {
+      if (buf) { mbar_wait(&bars[1], ph1); ph1 ^= 1; }
+      else { mbar_wait(&bars[0], ph0); ph0 ^= 1; }
+    } else {
+      cp_async_wait<1>();
+    }
     __syncthreads();
 
     if constexpr (OP != OP_SKETCH) {
       // ---- step A: partial W over this thread's rows for U columns at a time, then
-      // one batched transpose-reduce across the lanes sharing cg (lane bits >= log2 NCG).
-      constexpr int NV = U * TC;
-      const int nsteps = 5 - (31 - __clz(a.NCG));
-      const int cnt = (nsteps >= 31 - __clz(NV)) ? 1 : (NV >> nsteps);
-      for (int j0 = 0; j0 < a.b; j0 += U) {
+      // one batched transpose-reduce across the lanes sharing cg.
+      for (int jb = 0; jb < a.b; jb += U) {
         float mv[U][R];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (active) load_col<R>(Ms + (j0 + u) * a.pitch, rg, a.NRG, mv[u]);
-          else {
-#pragma unroll
-            for (int e = 0; e < R; ++e) mv[u][e] = 0.f;
-          }
-        }
+        for (int u = 0; u < U; ++u) load_col<R>(Ms + (jb + u) * pitch, rg, NRGp, mv[u]);
         float v[NV];
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -211,30 +263,31 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
           }
         int coff = 0;
 #pragma unroll
-        for (int s = 0; s < 5; ++s) {
+        for (int s = 0; s < NSTEPS; ++s) {
           const int mask = 16 >> s;
-          if (mask >= a.NCG) {
-            if ((NV >> s) >= 2) {
-              const bool up = (lane & mask) != 0;
+          if ((NV >> s) >= 2) {
+            const bool up = (lane & mask) != 0;
 #pragma unroll
-              for (int i = 0; i < (NV >> (s + 1)); ++i) {
-                const float send = up ? v[i] : v[i + (NV >> (s + 1))];
-                const float keep = up ? v[i + (NV >> (s + 1))] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-              }
-              if (up) coff += NV >> (s + 1);
-            } else {
-              v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+            for (int i = 0; i < (NV >> (s + 1)); ++i) {
+              const float send = up ? v[i] : v[i + (NV >> (s + 1))];
+              const float keep = up ? v[i + (NV >> (s + 1))] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
             }
+            if (up) coff += NV >> (s + 1);
+          } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
           }
         }
-        float* rw = red + ((size_t)warp * a.b + j0) * a.LC + cg * TC;
+        // lanes that differ only in the lowest reduced bits hold identical values: one writes
+        constexpr int LOWBITS = (NSTEPS > LOG_NV) ? ((1 << (NSTEPS - LOG_NV)) - 1) << LOG_NCG : 0;
+        if ((lane & LOWBITS) == 0) {
+          float* rw = red + ((size_t)warp * a.b + jb) * a.LC + cg * TC;
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
-          if (i < cnt) {
+          for (int i = 0; i < CNT; ++i) {
             const int f = coff + i;
             rw[(f / TC) * a.LC + (f % TC)] = v[i];
           }
+        }
       }
       __syncthreads();
       // ---- cross-warp sum in fixed order -> W ----
@@ -255,10 +308,20 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
         const int tg = chunk * a.LC + c;
         const int64_t jg = j0 + j;
         if (jg < a.m && tg < a.l) {
-          const int64_t aa = jg % a.Rprev;
-          const int64_t tmp = jg / a.Rprev;
-          const int64_t bb = tmp % a.nnext;
-          const int64_t cc = tmp / a.nnext;
+          int64_t aa, bb, cc;
+          if (a.m < (1ll << 31)) {
+            const uint32_t jj = (uint32_t)jg, rp = (uint32_t)a.Rprev, nn = (uint32_t)a.nnext;
+            const uint32_t tmp = jj / rp;
+            aa = jj - tmp * rp;
+            const uint32_t c32 = tmp / nn;
+            cc = c32;
+            bb = tmp - c32 * nn;
+          } else {
+            aa = jg % a.Rprev;
+            const int64_t tmp = jg / a.Rprev;
+            bb = tmp % a.nnext;
+            cc = tmp / a.nnext;
+          }
           const int64_t colo = aa + a.Rprev * (tg + (int64_t)a.l * cc);
           a.out[bb + a.ldnext * colo] = Wsm[j * a.LC + c];
           if (bb == a.nnext - 1)
@@ -267,55 +330,51 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
       }
     } else {
       // ---- step B: Y += M_J W_J on this thread's rows x TC columns, U columns at a time ----
-      if (active) {
-        const float* wrow = Wsm + cg * TC;
-        for (int j0 = 0; j0 < a.b; j0 += U) {
-          float mv[U][R];
-          float wv[U][TC];
+      const float* wrow = Wsm + cg * TC;
+      for (int jb = 0; jb < a.b; jb += U) {
+        float mv[U][R];
+        float wv[U][TC];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            load_col<R>(Ms + (j0 + u) * a.pitch, rg, a.NRG, mv[u]);
+        for (int u = 0; u < U; ++u) {
+          load_col<R>(Ms + (jb + u) * pitch, rg, NRGp, mv[u]);
 #pragma unroll
-            for (int c = 0; c < TC; c += 4) {
-              const float4 w4 = *reinterpret_cast<const float4*>(wrow + (j0 + u) * a.LC + c);
-              wv[u][c] = w4.x; wv[u][c + 1] = w4.y; wv[u][c + 2] = w4.z; wv[u][c + 3] = w4.w;
-            }
+          for (int c = 0; c < TC; c += 4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(wrow + (jb + u) * a.LC + c);
+            wv[u][c] = w4.x; wv[u][c + 1] = w4.y; wv[u][c + 2] = w4.z; wv[u][c + 3] = w4.w;
           }
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < R; ++e)
-#pragma unroll
-              for (int c = 0; c < TC; ++c) acc[e][c] = fmaf(mv[u][e], wv[u][c], acc[e][c]);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < R; ++e)
+#pragma unroll
+            for (int c = 0; c < TC; ++c) acc[e][c] = fmaf(mv[u][e], wv[u][c], acc[e][c]);
       }
     }
     __syncthreads();
     buf ^= 1;
   }
-  cp_async_wait<0>();
+  if (!a.bulk) cp_async_wait<0>();
 
   if constexpr (OP != OP_SHRINK) {
-    if (active) {
-      float* yp = a.Ypart + (int64_t)grp * a.yp_g;
+    float* yp = a.Ypart + (int64_t)grp * a.yp_g;
 #pragma unroll
-      for (int c = 0; c < TC; ++c) {
-        float* col = yp + (int64_t)(c_base + c) * a.n_rows;
+    for (int c = 0; c < TC; ++c) {
+      float* col = yp + (int64_t)(c_base + c) * a.n_rows;
 #pragma unroll
-        for (int e = 0; e < R; ++e) col[row_of<R>(rg, e, a.NRG)] = acc[e][c];
-      }
+      for (int e = 0; e < R; ++e) col[row_of<R>(rg, e, NRGp)] = acc[e][c];
     }
   }
 }
 
 // ------------------------------------------------------------------ host side
-template <int R, int TC>
+template <int R, int TC, int NCG>
 static cudaError_t launch_rt(const TileArgs& a, TileOp op, int grid, int nt, size_t smem,
                              cudaStream_t st) {
   void (*fn)(const TileArgs);
-  if (op == OP_SKETCH) fn = tile_kernel<R, TC, OP_SKETCH>;
-  else if (op == OP_POWER) fn = tile_kernel<R, TC, OP_POWER>;
-  else fn = tile_kernel<R, TC, OP_SHRINK>;
+  if (op == OP_SKETCH) fn = tile_kernel<R, TC, NCG, OP_SKETCH>;
+  else if (op == OP_POWER) fn = tile_kernel<R, TC, NCG, OP_POWER>;
+  else fn = tile_kernel<R, TC, NCG, OP_SHRINK>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, nt, smem, st>>>(a);
@@ -337,7 +396,29 @@ static size_t tile_smem(int b, int pitch, int LC, int NT) {
   return sizeof(float) * ((size_t)2 * b * pitch + (size_t)b * LC + (size_t)(NT / 32) * b * LC);
 }
 
-// Choose (R, TC, NCG, chunks, b, G) for an n x m view with l columns of Q.
+static bool valid_combo(int R, int TC, int NCG) {
+  const bool rt = (R == 1 || R == 2 || R == 4 || R == 8 || R == 16) && (TC == 4 || TC == 8) &&
+                  R * TC <= 64;
+  return rt && (NCG == 1 || NCG == 2 || NCG == 4 || NCG == 8);
+}
+
+static void finish_plan(TilePlan& p, int n, int l, int nsm) {
+  const int NRG = (n + p.R - 1) / p.R;
+  const int lanes = 32 / p.NCG;
+  p.NRG = (NRG + lanes - 1) / lanes * lanes;   // padded row groups (extra rows are zero)
+  p.NT = p.NRG * p.NCG;
+  p.LC = p.NCG * p.TC;
+  p.nchunks = (l + p.LC - 1) / p.LC;
+  p.pitch = p.R * p.NRG;
+  if (p.pitch % 4) p.pitch = (p.pitch + 3) / 4 * 4;
+  p.smem = tile_smem(p.b, p.pitch, p.LC, p.NT);
+  const int regs = 2 * p.R * p.TC + 48;
+  const int occ = std::max(1, std::min<int>(std::max(1, 65536 / (p.NT * regs)),
+                                            (int)((228 * 1024) / (p.smem + 2048))));
+  p.G = std::max(1, nsm * occ / p.nchunks);
+}
+
+// Choose (R, TC, NCG, chunks, b) for an n x m view with l columns of Q.
 TilePlan plan_tile(const View& v, int l, TileOp op, int nsm) {
   const int n = v.n;
   TilePlan best;
@@ -346,40 +427,32 @@ TilePlan plan_tile(const View& v, int l, TileOp op, int nsm) {
   const int TCs[] = {4, 8};
   for (int R : Rs) {
     for (int TC : TCs) {
-      if (R * TC > 64 || (R == 16 && TC == 8)) continue;
-      const int NRG = (n + R - 1) / R;
-      for (int NCG = 1; NCG <= 32; NCG <<= 1) {
-        const int lanes = 32 / NCG;
-        const int NRGp = (NRG + lanes - 1) / lanes * lanes;
-        const int NT = NRGp * NCG;
-        const int regs = 2 * R * TC + 40;
-        const int nt_max = std::min(256, (65536 / regs) / 32 * 32);
-        if (NT > nt_max || NT < 32) continue;
-        const int LC = NCG * TC;
-        const int nchunks = (l + LC - 1) / LC;
-        if (NCG > 1 && (nchunks * LC - l) >= LC / 2 && LC > 8) continue;  // mostly padding
-        int pitch = (R * NRG + 3) / 4 * 4;
-        // tile width: fill ~ 96 KB of double-buffered tile (2 CTAs/SM) or 200 KB (1 CTA/SM)
-        const int occ_regs = std::max(1, 65536 / (NT * regs));
-        int b = 64;
-        size_t budget = occ_regs >= 2 ? 100 * 1024 : 200 * 1024;
-        while (b > 4 && tile_smem(b, pitch, LC, NT) > budget) b -= 4;
-        if (tile_smem(b, pitch, LC, NT) > 220 * 1024) continue;
-        const size_t sm = tile_smem(b, pitch, LC, NT);
-        const int occ = std::max(1, std::min<int>(occ_regs, (int)((228 * 1024) / (sm + 1024))));
-        // cost model (cycles per column per SM, all chunks): FFMA / SMEM / SHFL
-        const double nw = NT / 32.0;
-        const double ffma = (op == OP_SKETCH ? 1.0 : (op == OP_POWER ? 2.0 : 1.0)) * nw * R * TC / 4.0;
+      for (int NCG = 1; NCG <= 8; NCG <<= 1) {
+        if (!valid_combo(R, TC, NCG)) continue;
+        TilePlan p;
+        p.R = R; p.TC = TC; p.NCG = NCG; p.b = 64;
+        finish_plan(p, n, l, nsm);
+        const int regs = 2 * R * TC + 48;
+        if (p.NT > 256 || p.NT < 32 || p.NT * regs > 65536) continue;
+        const int occ_regs = std::max(1, 65536 / (p.NT * regs));
+        const size_t budget = occ_regs >= 2 ? 100 * 1024 : 200 * 1024;
+        while (p.b > 4 && tile_smem(p.b, p.pitch, p.LC, p.NT) > budget) p.b -= 4;
+        if (tile_smem(p.b, p.pitch, p.LC, p.NT) > 220 * 1024) continue;
+        finish_plan(p, n, l, nsm);
+        // cost model, cycles per column per SM summed over chunks: issue slots of the
+        // FFMA work (+ reduction overhead) vs shared-memory wavefronts, padding included
+        const double nw = p.NT / 32.0;
+        const double rows_eff = (double)p.NRG * R;  // padded rows actually computed
+        const double ffma = (op == OP_POWER ? 2.0 : 1.0) * rows_eff * p.LC / 32.0 / 4.0;
+        const double lanes = 32.0 / NCG;
+        const double red = (op == OP_SKETCH) ? 0.0 : nw * (3.0 * TC * (1.0 - 1.0 / lanes) + 2.0) / 4.0;
         const double smem_wf = nw * ((op == OP_POWER ? 2.0 : 1.0) * R * lanes * 4.0 / 128.0 + TC / 4.0);
-        const double shfl = (op == OP_SKETCH) ? 0.0 : nw * (TC + 2.0);
-        double c = std::max(ffma, std::max(smem_wf, shfl)) * nchunks;
-        c *= 1.0 + 8.0 / b;   // per-tile barrier / reduction overhead
-        if (occ < 2) c *= 1.15;
+        double c = (std::max(ffma + red, smem_wf)) * p.nchunks;
+        c *= 1.0 + 6.0 / p.b;                        // per-tile barriers and cross-warp sum
+        if (occ_regs < 2 && nw < 8) c *= 1.3;        // too few warps to hide latency
         if (c < best_cost) {
           best_cost = c;
-          best.R = R; best.TC = TC; best.NRG = NRG; best.NCG = NCG; best.LC = LC;
-          best.nchunks = nchunks; best.NT = NT; best.b = b; best.pitch = pitch; best.smem = sm;
-          best.G = std::max(1, nsm * occ / nchunks);
+          best = p;
         }
       }
     }
@@ -389,18 +462,10 @@ TilePlan plan_tile(const View& v, int l, TileOp op, int nsm) {
   const char* ov = getenv(names[op]);
   if (!ov) ov = getenv("RTK_PLAN");
   int oR, oTC, oNCG, ob;
-  if (ov && sscanf(ov, "%d,%d,%d,%d", &oR, &oTC, &oNCG, &ob) == 4) {
-    const int NRG = (n + oR - 1) / oR;
-    const int lanes = 32 / oNCG;
-    const int NRGp = (NRG + lanes - 1) / lanes * lanes;
-    best.R = oR; best.TC = oTC; best.NCG = oNCG; best.NRG = NRG; best.LC = oNCG * oTC;
-    best.nchunks = (l + best.LC - 1) / best.LC; best.NT = NRGp * oNCG; best.b = ob;
-    best.pitch = (oR * NRG + 3) / 4 * 4;
-    best.smem = tile_smem(ob, best.pitch, best.LC, best.NT);
-    const int regs = 2 * oR * oTC + 40;
-    const int occ = std::max(1, std::min<int>(std::max(1, 65536 / (best.NT * regs)),
-                                              (int)((228 * 1024) / (best.smem + 1024))));
-    best.G = std::max(1, nsm * occ / best.nchunks);
+  if (ov && sscanf(ov, "%d,%d,%d,%d", &oR, &oTC, &oNCG, &ob) == 4 && valid_combo(oR, oTC, oNCG) &&
+      ob % 4 == 0 && ob > 0) {
+    best.R = oR; best.TC = oTC; best.NCG = oNCG; best.b = ob;
+    finish_plan(best, n, l, nsm);
   }
   best.ntiles = (v.m() + best.b - 1) / best.b;
   if (best.G > best.ntiles) best.G = (int)best.ntiles;
@@ -417,19 +482,21 @@ cudaError_t launch_tile(const TileLaunch& L, cudaStream_t st) {
   a.M = L.v.base; a.P = L.v.P; a.S = L.v.S; a.sp = L.v.sp; a.si = L.v.si; a.ss = L.v.ss;
   a.m = L.v.m(); a.n = L.v.n;
   a.n4 = (L.v.n + 3) / 4 * 4;
-  a.vec = (L.v.P == 1 && L.v.si == 1 && (L.v.ss % 4) == 0 && L.v.ss >= a.n4 &&
-           ((uintptr_t)L.v.base % 16) == 0) ? 1 : 0;
-  a.n_rows = p.n_rows(); a.pitch = p.pitch; a.NRG = p.NRG; a.NCG = p.NCG; a.LC = p.LC;
+  a.bulk = (L.v.P == 1 && L.v.si == 1 && (L.v.ss % 4) == 0 && L.v.ss >= a.n4 && a.n4 <= p.pitch &&
+            ((uintptr_t)L.v.base % 16) == 0) ? 1 : 0;
+  a.n_rows = p.n_rows(); a.pitch = p.pitch; a.NRG = p.NRG; a.LC = p.LC;
   a.nchunks = p.nchunks; a.G = p.G; a.b = p.b; a.ntiles = p.ntiles; a.l = L.l;
   a.Q = L.Q; a.qld = L.qld; a.Ypart = L.Ypart; a.yp_g = (int64_t)p.ltot() * p.n_rows();
   a.seed = L.seed; a.mode = L.mode; a.out = L.out; a.Rprev = L.Rprev; a.nnext = L.nnext;
   a.ldnext = L.ldnext;
   const int grid = p.G * p.nchunks;
   const size_t smem = tile_smem(p.b, p.pitch, p.LC, p.NT);
-#define RTK_CASE(R_, TC_) \
-  if (p.R == R_ && p.TC == TC_) return launch_rt<R_, TC_>(a, L.op, grid, p.NT, smem, st);
-  RTK_CASE(1, 4) RTK_CASE(1, 8) RTK_CASE(2, 4) RTK_CASE(2, 8) RTK_CASE(4, 4) RTK_CASE(4, 8)
-  RTK_CASE(8, 4) RTK_CASE(8, 8) RTK_CASE(16, 4)
+#define RTK_CASE(R_, TC_, NCG_) \
+  if (p.R == R_ && p.TC == TC_ && p.NCG == NCG_) return launch_rt<R_, TC_, NCG_>(a, L.op, grid, p.NT, smem, st);
+#define RTK_CASES(R_, TC_) RTK_CASE(R_, TC_, 1) RTK_CASE(R_, TC_, 2) RTK_CASE(R_, TC_, 4) RTK_CASE(R_, TC_, 8)
+  RTK_CASES(1, 4) RTK_CASES(1, 8) RTK_CASES(2, 4) RTK_CASES(2, 8) RTK_CASES(4, 4) RTK_CASES(4, 8)
+  RTK_CASES(8, 4) RTK_CASES(8, 8) RTK_CASES(16, 4)
+#undef RTK_CASES
 #undef RTK_CASE
   return cudaErrorInvalidConfiguration;
 }
