@@ -146,6 +146,7 @@ class Report:
     q_used: list
     fallback: int
     numeric: int
+    jacobi_sweeps: list = None   # sweeps of each mode's last Jacobi solve (diagnostics)
 
 
 class _WorkspaceCache:
@@ -221,7 +222,8 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     ls = [r + p for r in ranks]
     r_obj = Report([list(at[k * q:(k + 1) * q]) for k in range(d)],
                    [list(sg[k * 128:k * 128 + ls[k]]) for k in range(d)],
-                   list(qu), rep.fallback, rep.numeric)
+                   list(qu), rep.fallback, rep.numeric,
+                   [[sg[k * 128 + 100 + s] for s in range(q + 1)] for k in range(d)])
     return core, U, r_obj
 
 
