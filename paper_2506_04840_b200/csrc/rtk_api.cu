@@ -140,20 +140,44 @@ View shrink_view(const Problem& P, int k, const float* A, const float* buf) {
 }
 
 struct Layout {
+  size_t planes = 0, wbuf = 0;
+  int64_t ldw = 0;
+  std::vector<char> tc_range, tc_shrink;
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
   size_t shr_elems = 0;
   std::vector<TilePlan> sk, pw, sh;
 };
 
-Layout plan(const Problem& P, int nsm) {
+Layout plan(const Problem& P, int nsm, const float* A, int path) {
   Layout L;
-  size_t ypart = 0, nl = 0, qsz = 0, gp = 0, ll = 0, lmax = 0;
+  size_t ypart = 0, nl = 0, qsz = 0, gp = 0, ll = 0, lmax = 0, planes = 0, wbuf = 0;
   L.sk.resize(P.d); L.pw.resize(P.d); L.sh.resize(P.d);
+  L.tc_range.assign(P.d, 0);
+  L.tc_shrink.assign(P.d, 0);
   size_t shr = 0;
+  int64_t ldw = 4;
   for (int k = 0; k < P.d; ++k) {
     const int l = P.ranks[k] + P.p;
     View rv = range_view(P, k, nullptr, nullptr);
+    // tcgen05 eligibility is a property of the view's shape / stride (alignment of the real
+    // pointers is re-checked at launch time; A's base decides for the views that read it)
+    View rvp = rv;
+    rvp.base = (!P.seq || k == 0) ? A : (const float*)nullptr;
+    View svp = shrink_view(P, k, nullptr, nullptr);
+    svp.base = k == 0 ? A : (const float*)nullptr;
+    if (path != 1) {
+      L.tc_range[k] = tc_supported(rvp, l) ? 1 : 0;
+      L.tc_shrink[k] = tc_supported(svp, P.ranks[k]) ? 1 : 0;
+    }
+    if (L.tc_range[k]) {
+      const int N = tc_npad(l), nit = (rv.n + 127) / 128;
+      ypart = std::max(ypart, (size_t)nsm * N * nit * 128);
+      planes = std::max(planes, (size_t)2 * N * pad4(rv.n));
+      ldw = std::max<int64_t>(ldw, pad4(rv.m()));
+      wbuf = std::max(wbuf, (size_t)2 * N * pad4(rv.m()));
+    }
+    if (L.tc_shrink[k]) planes = std::max(planes, (size_t)2 * tc_npad(P.ranks[k]) * pad4(rv.n));
     L.sk[k] = plan_tile(rv, l, OP_SKETCH, nsm);
     L.pw[k] = plan_tile(rv, l, OP_POWER, nsm);
     View sv = shrink_view(P, k, nullptr, nullptr);
@@ -177,6 +201,9 @@ Layout plan(const Problem& P, int nsm) {
   L.shr_elems = shr;
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off += align_up(std::max<size_t>(bytes, 16)); return o; };
+  L.ldw = ldw;
+  L.planes = take(planes * 4);
+  L.wbuf = take(wbuf * 4);
   L.ypart = take(ypart * 4);
   L.y = take(nl * 8);
   L.q1 = take(nl * 8);
@@ -224,8 +251,24 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   B.sighat = (double*)(ws + L.sighat);
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
   const uint32_t mode1 = (uint32_t)(k + 1);
+  const bool tc = L.tc_range[k] && tc_supported(v, l);
   for (int step = 0; step <= P.q; ++step) {
     const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
+    if (tc) {
+      ProfScope ps(step == 0 ? 0 : 1, k, st);
+      float* planes = (float*)(ws + L.planes);
+      float* W = (float*)(ws + L.wbuf);
+      if (step == 0) {
+        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, num_sms(), st));
+        g_launches += 1;
+      } else {
+        RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));
+        RTK_CK(tc_op1(v, l, planes, W, L.ldw, false, nullptr, 1, 1, 1, st));
+        RTK_CK(tc_op2(v, l, W, L.ldw, false, 0, 0, B.Ypart, num_sms(), st));
+        g_launches += 3;
+      }
+      B.G = num_sms(); B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
+    } else {
     TileLaunch T;
     T.v = v;
     T.op = step == 0 ? OP_SKETCH : OP_POWER;
@@ -239,8 +282,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     {
       ProfScope ps(step == 0 ? 0 : 1, k, st);
       RTK_CK(launch_tile(T, st));
+      g_launches += 1;
     }
     B.G = tp.G; B.ltot = tp.ltot(); B.n_rows = tp.n_rows();
+    }
     {
       ProfScope ps(3, k, st);
       RTK_CK(launch_reduce_gram(B, step > 0, st));
@@ -257,7 +302,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
 }
 
 // G x_k U_k^T written as the next unfolding (or the canonical core after mode d).
-int run_shrink(const Problem& P, const Layout& L, int k, const View& v, const float* Uk, float* out,
+int run_shrink(const Problem& P, const Layout& L, char* ws, int k, const View& v, const float* Uk, float* out,
                cudaStream_t st) {
   TileLaunch T;
   T.v = v;
@@ -273,6 +318,13 @@ int run_shrink(const Problem& P, const Layout& L, int k, const View& v, const fl
   else { T.nnext = 1; T.ldnext = 1; }
   T.out = out;
   ProfScope ps(2, k, st);
+  if (L.tc_shrink[k] && tc_supported(v, P.ranks[k])) {
+    float* planes = (float*)(ws + L.planes);
+    RTK_CK(tc_split(nullptr, Uk, v.n, P.ranks[k], planes, st));
+    RTK_CK(tc_op1(v, P.ranks[k], planes, nullptr, 0, true, out, T.Rprev, T.nnext, T.ldnext, st));
+    g_launches += 2;
+    return RTK_OK;
+  }
   RTK_CK(launch_tile(T, st));
   g_launches += 1;
   return RTK_OK;
@@ -294,7 +346,11 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   if ((uintptr_t)A % 4) return fail(RTK_ERR_ALIGN, "A must be 4-byte aligned");
   if (opt.pve_tol > 0.0) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) is not implemented on the GPU path yet");
   cudaStream_t st = (cudaStream_t)stream;
-  const Layout L = plan(P, num_sms());
+  if (opt.path < 0 || opt.path > 2) return fail(RTK_ERR_ARG, "path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
+  const Layout L = plan(P, num_sms(), A, opt.path);
+  if (opt.path == 2)
+    for (int k = 0; k < d; ++k)
+      if (!L.tc_range[k]) return fail(RTK_ERR_SHAPE, "tcgen05 path unavailable for mode " + std::to_string(k + 1));
   char* ws = (char*)ws_in;
   bool own = false;
   if (!ws) {
@@ -315,7 +371,7 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
       rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
       if (rc) return rc;
       const View sv = shrink_view(P, k, A, cur);
-      rc = run_shrink(P, L, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
+      rc = run_shrink(P, L, ws, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
       if (rc) return rc;
     }
   } else {
@@ -329,7 +385,7 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
     for (int k = 0; k < d; ++k) {
       const float* cur = k == 0 ? A : shr[(k - 1) & 1];
       const View sv = shrink_view(P, k, A, cur);
-      rc = run_shrink(P, L, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
+      rc = run_shrink(P, L, ws, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
       if (rc) return rc;
     }
   }
@@ -394,7 +450,7 @@ size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const i
   P.dims.assign(dims, dims + d);
   P.ranks.assign(ranks, ranks + d);
   if (validate(P)) return 0;
-  return plan(P, num_sms()).total;
+  return plan(P, num_sms(), nullptr, 0).total;
 }
 
 int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out, void* stream) {
@@ -412,6 +468,23 @@ int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float
   cudaStream_t st = (cudaStream_t)stream;
   View v;
   v.base = M; v.n = (int)n; v.P = 1; v.S = m; v.sp = 1; v.si = 1; v.ss = ld;
+  const char* pe = getenv("RTK_PATH");
+  if (!(pe && std::string(pe) == "ffma") && tc_supported(v, l)) {
+    const int N = tc_npad(l), nit = (int)((n + 127) / 128), G = num_sms();
+    const int64_t ldw = pad4(m);
+    float *planes = nullptr, *W = nullptr, *yp = nullptr;
+    RTK_CK(cudaMallocAsync((void**)&planes, (size_t)2 * N * pad4(n) * 4, st));
+    RTK_CK(cudaMallocAsync((void**)&W, (size_t)2 * N * ldw * 4, st));
+    RTK_CK(cudaMallocAsync((void**)&yp, (size_t)G * N * nit * 128 * 4, st));
+    RTK_CK(tc_split(nullptr, Q, (int)n, l, planes, st));
+    RTK_CK(tc_op1(v, l, planes, W, ldw, false, nullptr, 1, 1, 1, st));
+    RTK_CK(tc_op2(v, l, W, ldw, false, 0, 0, yp, G, st));
+    RTK_CK(launch_sum_partials(yp, G, N, nit * 128, (int)n, l, Y, st));
+    RTK_CK(cudaFreeAsync(planes, st));
+    RTK_CK(cudaFreeAsync(W, st));
+    RTK_CK(cudaFreeAsync(yp, st));
+    return RTK_OK;
+  }
   TileLaunch T;
   T.v = v;
   T.op = OP_POWER;

@@ -89,4 +89,13 @@ cudaError_t launch_sum_partials(const float* Ypart, int G, int ltot, int n_rows,
 
 int num_sms();
 
+// ---- tcgen05 3xTF32 path (rtk_tc.cu) -------------------------------------------
+int tc_npad(int l);                                   // l padded to the UMMA N (16..64), 0 if > 64
+bool tc_supported(const View& v, int l);              // contiguous column-major view, sm_100
+cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* planes, cudaStream_t st);
+cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,
+                   int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st);
+cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
+                   float* Ypart, int G, cudaStream_t st);
+
 }  // namespace rtk

@@ -50,8 +50,10 @@ def check(a, ranks, p, q, seed, sequential, gaps=None, alpha_rtol=1e-3):
     return re_g, re_o
 
 
+@pytest.mark.parametrize("path", ["ffma", "tc"])
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
-def test_config_parity(cfg):
+def test_config_parity(cfg, path, monkeypatch):
+    monkeypatch.setenv("RTK_PATH", path)
     c = CONFIGS[cfg]
     a = make_config_tensor(cfg)
     check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], c["algo"] == "rsthosvd")
