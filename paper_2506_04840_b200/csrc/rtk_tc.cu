@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op1_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    // ---------------- UMMA issuer
-    if (lane == 0) {
+    // ---------------- UMMA issuer (whole warp, uniform; one lane elected per instruction)
+    {
+      const uint64_t d0 = sdesc_sw128(smem_addr(sm), 16, 1024);   // stage 0, A hi; offsets added below
       int64_t it = 0;
       int lt = 0;
       for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++lt) {
@@ -122,20 +123,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op1_kernel(const __grid_cons
           bar_wait(&full[s], ph);
           bar_wait(&lofull[s], ph);
           tc_fence_after();
-          const uint32_t base = smem_addr(sm + s * STAGE);
+          const uint64_t ds = d0 + (uint64_t)((s * STAGE) >> 4);
 #pragma unroll
           for (int k8 = 0; k8 < 4; ++k8) {
-            const uint64_t ahi = sdesc_sw128(base + k8 * 32, 16, 1024);
-            const uint64_t alo = sdesc_sw128(base + kTileBytesA + k8 * 32, 16, 1024);
-            const uint64_t bhi = sdesc_sw128(base + 2 * kTileBytesA + k8 * 32, 16, 1024);
-            const uint64_t blo = sdesc_sw128(base + 2 * kTileBytesA + BB + k8 * 32, 16, 1024);
-            umma_tf32(d, alo, bhi, IDESC, (kc | k8) != 0);
-            umma_tf32(d, ahi, blo, IDESC, 1);
-            umma_tf32(d, ahi, bhi, IDESC, 1);
+            const uint64_t ahi = ds + (k8 * 32 >> 4);
+            const uint64_t alo = ds + ((kTileBytesA + k8 * 32) >> 4);
+            const uint64_t bhi = ds + ((2 * kTileBytesA + k8 * 32) >> 4);
+            const uint64_t blo = ds + ((2 * kTileBytesA + BB + k8 * 32) >> 4);
+            umma_tf32_e(d, alo, bhi, IDESC, (kc | k8) != 0);
+            umma_tf32_e(d, ahi, blo, IDESC, 1);
+            umma_tf32_e(d, ahi, bhi, IDESC, 1);
           }
-          umma_commit(&empty[s]);
+          umma_commit_e(&empty[s]);
         }
-        umma_commit(&accf[b]);
+        umma_commit_e(&accf[b]);
       }
     }
   } else if (warp < 6) {
@@ -269,39 +270,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
+      // MN-major A (SW128_BASE32B): K-step k8 = rows 8k8..8k8+7 of j at +1024*k8; MN groups of
+      // 32 i at +4096 (LBO); 4-row K atoms at +512 (SBO).  Base descriptors once; offsets added.
+      const uint64_t a0 = sdesc_sw128(smem_addr(smA), 4096, 512, kLayoutSW128Base32B);
+      const uint64_t b0 = sdesc_sw128(smem_addr(smB), 16, 1024);
       int64_t ia = 0;
       for (int64_t kc = k0; kc < k1; ++kc) {
         const int64_t ib = kc - k0;
         const int sb = (int)(ib % SB);
         bar_wait(&fullB[sb], (uint32_t)((ib / SB) & 1));
         tc_fence_after();
-        const uint32_t bbase = smem_addr(smB + sb * STB);
+        const uint64_t bs = b0 + (uint64_t)((sb * STB) >> 4);
         for (int itile = 0; itile < a.nit; ++itile, ++ia) {
           const int s = (int)(ia % SA);
           const uint32_t ph = (uint32_t)((ia / SA) & 1);
           bar_wait(&fullA[s], ph);
           bar_wait(&loA[s], ph);
           tc_fence_after();
-          const uint32_t abase = smem_addr(smA + s * STA);
+          const uint64_t as = a0 + (uint64_t)((s * STA) >> 4);
           const uint32_t d = tbase + itile * N;
 #pragma unroll
           for (int k8 = 0; k8 < 4; ++k8) {
-            // MN-major A (SW128_BASE32B): K-step k8 = rows 8k8..8k8+7 of j at +1024*k8; MN groups of
-            // 32 i at +4096 (LBO); 4-row K atoms at +512 (SBO)
-            const uint64_t ahi = sdesc_sw128(abase + k8 * 1024, 4096, 512, kLayoutSW128Base32B);
-            const uint64_t alo = sdesc_sw128(abase + kTileBytesA + k8 * 1024, 4096, 512, kLayoutSW128Base32B);
-            const uint64_t bhi = sdesc_sw128(bbase + k8 * 32, 16, 1024);
-            const uint64_t blo = sdesc_sw128(bbase + BB + k8 * 32, 16, 1024);
-            umma_tf32(d, alo, bhi, IDESC, (kc != k0) || (k8 != 0));
-            umma_tf32(d, ahi, blo, IDESC, 1);
-            umma_tf32(d, ahi, bhi, IDESC, 1);
+            const uint64_t ahi = as + ((k8 * 1024) >> 4);
+            const uint64_t alo = as + ((kTileBytesA + k8 * 1024) >> 4);
+            const uint64_t bhi = bs + ((k8 * 32) >> 4);
+            const uint64_t blo = bs + ((BB + k8 * 32) >> 4);
+            umma_tf32_e(d, alo, bhi, IDESC, (kc != k0) || (k8 != 0));
+            umma_tf32_e(d, ahi, blo, IDESC, 1);
+            umma_tf32_e(d, ahi, bhi, IDESC, 1);
           }
-          umma_commit(&emptyA[s]);
+          umma_commit_e(&emptyA[s]);
         }
-        umma_commit(&emptyB[sb]);
+        umma_commit_e(&emptyB[sb]);
       }
-      umma_commit(&accf);
+      umma_commit_e(&accf);
     }
   } else if (warp < 6) {
     const int tid = threadIdx.x - 64;    // 0..127
