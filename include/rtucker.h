@@ -138,6 +138,11 @@ typedef struct rtk_prof_stats {
 RTK_API int rtk_profile_begin(void);
 RTK_API int rtk_profile_end(rtk_prof_stats* out);
 
+/* Diagnostics: when dev_buf (device, 8*8*16 doubles) is non-NULL, every l <= 64 small-solve
+ * launch of later calls writes its phase clock counts to dev_buf[((mode*8)+step)*16 + ...]
+ * (SM cycles, CTA 0 of the cluster).  NULL disables.  Not needed for normal use. */
+RTK_API int rtk_debug_step_clocks(void* dev_buf);
+
 /* Thread-local message for the last non-zero status. */
 RTK_API const char* rtk_last_error(void);
 

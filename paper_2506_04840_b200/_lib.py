@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_omega",
-                 "rtk_power_step", "rtk_profile_begin", "rtk_profile_end", "rtk_last_error",
-                 "rtk_version"]
+                 "rtk_power_step", "rtk_profile_begin", "rtk_profile_end", "rtk_debug_step_clocks",
+                 "rtk_last_error", "rtk_version"]
 
 RTK_STATUS = {0: "RTK_OK", 1: "RTK_ERR_ARG", 2: "RTK_ERR_SHAPE", 3: "RTK_ERR_ALIGN",
               4: "RTK_ERR_WORKSPACE", 5: "RTK_ERR_CUDA", 6: "RTK_ERR_NUMERIC"}
@@ -78,6 +78,8 @@ def load_library():
     lib.rtk_profile_begin.restype = ctypes.c_int
     lib.rtk_profile_end.argtypes = [ctypes.POINTER(ProfStats)]
     lib.rtk_profile_end.restype = ctypes.c_int
+    lib.rtk_debug_step_clocks.argtypes = [vp]
+    lib.rtk_debug_step_clocks.restype = ctypes.c_int
     lib.rtk_last_error.restype = ctypes.c_char_p
     lib.rtk_version.restype = ctypes.c_char_p
     _LIB = lib

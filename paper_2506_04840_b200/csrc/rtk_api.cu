@@ -145,6 +145,7 @@ struct Layout {
   std::vector<char> tc_range, tc_shrink;
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
+  size_t g2part = 0, gsum = 0, amax = 0;
   size_t shr_elems = 0;
   std::vector<TilePlan> sk, pw, sh;
 };
@@ -188,6 +189,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
     nl = std::max(nl, n * l);
     qsz = std::max(qsz, n * l);
     gp = std::max(gp, (size_t)((n + 63) / 64) * l * (l + 1) / 2);
+    if (l <= kSolveLMax) gp = std::max(gp, solve_gpart_doubles((int)n, l));
     ll = std::max(ll, (size_t)l * l);
     lmax = std::max(lmax, (size_t)l);
     if (k + 1 < P.d) {
@@ -217,10 +219,38 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.sigma = take((size_t)P.d * 128 * 8);
   L.status = take((size_t)P.d * 4 * 4);
   L.sighat = take(lmax * 8);
+  L.g2part = take((size_t)8 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);
+  L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
+  L.amax = take((size_t)8 * 2 * kSolveLMax * 8);
   L.shr0 = take(shr * 4);
   L.shr1 = take(shr * 4);
   L.total = off;
   return L;
+}
+
+// Side stream + events (per device) for the deferred shift update (alpha_kernel, rtk_solve.cu):
+// it overlaps the next power step's streaming kernels, which then leave one SM free.
+struct Side {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_step = nullptr, ev_alpha = nullptr;
+};
+cudaError_t side_streams(Side** out) {
+  static std::mutex mu;
+  static Side S[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  Side& s = S[dev];
+  if (!s.aux) {
+    e = cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.ev_alpha, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *out = &s;
+  return cudaSuccess;
 }
 
 #define RTK_CK(x)                                                                          \
@@ -249,25 +279,34 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   B.sigma = (double*)(ws + L.sigma) + (size_t)k * 128;
   B.status = (int*)(ws + L.status) + 4 * k;
   B.sighat = (double*)(ws + L.sighat);
+  B.g2part = (double*)(ws + L.g2part);
+  B.gsum = (double*)(ws + L.gsum);
+  B.amax = (double*)(ws + L.amax);
+  const bool fast = l <= kSolveLMax;   // cluster small solver (rtk_solve.cu)
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
   const uint32_t mode1 = (uint32_t)(k + 1);
   const bool tc = L.tc_range[k] && tc_supported(v, l);
+  Side* side = nullptr;
+  const bool defer = fast && tc && P.q > 1;   // deferred shift updates on the side stream
+  if (defer) RTK_CK(side_streams(&side));
+  bool pending = false;                       // an alpha_kernel is in flight on side->aux
   for (int step = 0; step <= P.q; ++step) {
     const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
     if (tc) {
       ProfScope ps(step == 0 ? 0 : 1, k, st);
       float* planes = (float*)(ws + L.planes);
       float* W = (float*)(ws + L.wbuf);
+      const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
       if (step == 0) {
-        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, num_sms(), st));
+        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G, st));
         g_launches += 1;
       } else {
-        RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));
-        RTK_CK(tc_op1(v, l, planes, W, L.ldw, false, nullptr, 1, 1, 1, st));
-        RTK_CK(tc_op2(v, l, W, L.ldw, false, 0, 0, B.Ypart, num_sms(), st));
+        if (!fast) RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));   // else: written by step_kernel
+        RTK_CK(tc_op1(v, l, planes, W, L.ldw, false, nullptr, 1, 1, 1, st, G));
+        RTK_CK(tc_op2(v, l, W, L.ldw, false, 0, 0, B.Ypart, G, st));
         g_launches += 3;
       }
-      B.G = num_sms(); B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
+      B.G = G; B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
     } else {
     TileLaunch T;
     T.v = v;
@@ -286,18 +325,40 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     }
     B.G = tp.G; B.ltot = tp.ltot(); B.n_rows = tp.n_rows();
     }
-    {
+    if (fast) {
+      ProfScope ps(3, k, st);
+      float* planes = tc ? (float*)(ws + L.planes) : nullptr;
+      if (pending) {   // the previous step's alpha is needed by this reduce (Y = M M^T Q - alpha Q)
+        RTK_CK(cudaStreamWaitEvent(st, side->ev_alpha, 0));
+        pending = false;
+      }
+      RTK_CK(launch_reduce_gram2(B, step > 0, st));
+      const bool dstep = defer && step > 0 && step < P.q;
+      RTK_CK(launch_step(B, step, P.q, shift, step == P.q ? Uk : nullptr, seed, mode1, planes, tc_npad(l),
+                         (int)pad4(n), dstep, st));
+      g_launches += 2;
+      if (dstep) {
+        RTK_CK(cudaEventRecord(side->ev_step, st));
+        RTK_CK(cudaStreamWaitEvent(side->aux, side->ev_step, 0));
+        RTK_CK(launch_alpha(B, step, shift, side->aux));
+        RTK_CK(cudaEventRecord(side->ev_alpha, side->aux));
+        pending = true;
+        g_launches += 1;
+      }
+    } else {
       ProfScope ps(3, k, st);
       RTK_CK(launch_reduce_gram(B, step > 0, st));
       RTK_CK(launch_eig(B, step, P.q, shift, 0.0, st));
       RTK_CK(launch_apply(B, seed, mode1, step, st));
       RTK_CK(launch_chol(B, st));
       RTK_CK(launch_apply2(B, st));
+      g_launches += 6;
     }
-    g_launches += 6;
   }
-  RTK_CK(launch_final_u(B, Uk, st));
-  g_launches += 1;
+  if (!fast) {
+    RTK_CK(launch_final_u(B, Uk, st));
+    g_launches += 1;
+  }
   return RTK_OK;
 }
 
@@ -534,6 +595,11 @@ int rtk_profile_end(rtk_prof_stats* out) {
   g_prof.clear();
   if (out) out->launches = g_launches.load();
   return rc;
+}
+
+int rtk_debug_step_clocks(void* dev_buf) {
+  rtk::g_step_dbg = (double*)dev_buf;
+  return RTK_OK;
 }
 
 const char* rtk_last_error(void) { return g_err.c_str(); }

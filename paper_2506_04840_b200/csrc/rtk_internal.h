@@ -72,6 +72,10 @@ struct ModeBufs {
   double* sigma = nullptr;  // [128] final sigma estimates
   int* status = nullptr;    // [0]=numeric, [1]=fallback count, [2]=q_used, [3]=pve_stop
   double* sighat = nullptr; // [l] B.1 sigma-hat
+  // cluster solver (rtk_solve.cu, l <= 64)
+  double* g2part = nullptr; // [8][np] second-pass Gram partials
+  double* gsum = nullptr;   // [np]
+  double* amax = nullptr;   // [8][128] sign-pin argmax exchange
 };
 
 cudaError_t launch_reduce_gram(const ModeBufs& B, bool power, cudaStream_t st);
@@ -89,12 +93,21 @@ cudaError_t launch_sum_partials(const float* Ypart, int G, int ltot, int n_rows,
 
 int num_sms();
 
+// ---- cluster small solver (rtk_solve.cu), l <= 64 ------------------------------
+constexpr int kSolveLMax = 64;
+extern double* g_step_dbg;
+size_t solve_gpart_doubles(int n, int l);      // Gram partials of reduce_gram_kernel
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st);
+cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
+                        float* planes, int pN, int pld, bool defer_alpha, cudaStream_t st);
+cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t st);
+
 // ---- tcgen05 3xTF32 path (rtk_tc.cu) -------------------------------------------
 int tc_npad(int l);                                   // l padded to the UMMA N (16..64), 0 if > 64
 bool tc_supported(const View& v, int l);              // contiguous column-major view, sm_100
 cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* planes, cudaStream_t st);
 cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,
-                   int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st);
+                   int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st, int max_ctas = 0);
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
                    float* Ypart, int G, cudaStream_t st);
 

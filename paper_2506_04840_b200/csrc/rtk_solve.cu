@@ -1,0 +1,1142 @@
+// rtk_solve.cu -- low-latency float64 "small solves" of one sketch / power step, l <= 64.
+//
+// After a streaming kernel has produced per-CTA fp32 partial sums of M (M^T Q) (or M Omega_k),
+// one step of Alg. 3/4 finishes in TWO launches:
+//
+//   reduce_gram_kernel  (whole GPU, 8 rows per CTA)
+//       Y = sum_g Ypart[g] - alpha Q           fixed g order, fp64 (Alg. 3/4 line 7's "- alpha Q")
+//       per-block packed upper Gram  Y_b^T Y_b
+//   step_kernel         (one thread-block cluster of C <= 8 CTAs, 256 threads each)
+//       G = sum_b Gram_b                        (cluster-parallel sum, fixed order)
+//       every CTA redundantly (identical inputs -> identical results) factors the l x l G:
+//         span path   (sketch / non-final power step):  G = R^T R, T = R^{-1};
+//                      a second CholQR pass only if eps * kappa_F(R)^2 > 1e-10
+//         shift       (power steps): Sigma_ll = sqrt(lambda_min(G)) by Householder
+//                      tridiagonalisation + Sturm multisection; alpha <- (Sigma_ll + alpha)/2
+//                      if Sigma_ll > alpha (degenerate guard SPEC.md:347)
+//         eigen path  (final step, or Cholesky breakdown): G = V Lambda V^T via tridiagonalisation,
+//                      all-eigenvalue Sturm bisection, inverse iteration and back-transformation;
+//                      T = V Lambda^{-1/2} in descending order (left singular vectors of Y, which
+//                      U_k = Q(:,1:r_k) needs); null columns completed by a Philox
+//                      block; always followed by a second CholQR pass
+//       each CTA: Q = Y T (and Q1 T2) on its own rows; outputs fp64 Q, fp32 shadow, the 3xTF32
+//       B-operand planes of the next power step, and (final step) U_k with the SPEC.md:232 sign
+//       pin (cluster-wide argmax).
+//
+// All arithmetic is float64; every reduction has a fixed order, so repeated
+// runs are bit-identical.  Cross-CTA data goes through global memory (L2) ordered by
+// barrier.cluster (release/acquire), read with ld.global.cg.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "rtk_gauss.cuh"
+#include "rtk_internal.h"
+#include "rtk_sm100.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rtk {
+
+constexpr int kSL = 64;        // max l of this solver
+constexpr int kLD = 65;        // leading dimension of the l x l fp64 shared matrices
+constexpr int kMLD = 66;       // leading dimension of T (even: 16-byte double2 rows)
+constexpr int kST = 256;       // threads per CTA
+constexpr int kRBr = 8;        // rows per reduce_gram CTA
+constexpr int kChunk = 64;     // rows per product chunk in step_kernel
+constexpr int kMaxC = 8;       // cluster size (portable maximum)
+
+__device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
+  int t = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+  while (t * (t + 1) / 2 > e) --t;
+  while ((t + 1) * (t + 2) / 2 <= e) ++t;
+  c2 = t;
+  c1 = e - t * (t + 1) / 2;
+}
+
+// =============================================================== reduce + Gram partials
+__global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restrict__ Ypart, int G, int ltot,
+                                                         int n_rows, int n, int l,
+                                                         const double* __restrict__ Qd,
+                                                         const double* __restrict__ alpha, int power,
+                                                         double* __restrict__ Y, double* __restrict__ gpart) {
+  __shared__ double Ys[kRBr][kSL + 1];
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.x * kRBr;
+  const int rows = min(kRBr, n - i0);
+  const double a = power ? *alpha : 0.0;
+  const int64_t gs = (int64_t)ltot * n_rows;
+  for (int idx = tid; idx < kRBr * l; idx += kST) {
+    const int c = idx / kRBr, ii = idx % kRBr;
+    double s = 0.0;
+    if (ii < rows) {
+      const int i = i0 + ii;
+      const float* src = Ypart + (int64_t)c * n_rows + i;
+      int g = 0;
+      for (; g + 8 <= G; g += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(g + u) * gs);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += (double)v[u];
+      }
+      for (; g < G; ++g) s += (double)__ldcg(src + (int64_t)g * gs);
+      if (power) s -= a * Qd[(int64_t)c * n + i];
+      Y[(int64_t)c * n + i] = s;
+    }
+    Ys[ii][c] = s;
+  }
+  __syncthreads();
+  const int np = l * (l + 1) / 2;
+  double* gp = gpart + (int64_t)blockIdx.x * np;
+  for (int e = tid; e < np; e += kST) {
+    int c1, c2;
+    unpack_upper(e, c1, c2);
+    double s = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < kRBr; ++ii) s += Ys[ii][c1] * Ys[ii][c2];
+    gp[e] = s;
+  }
+}
+
+// =============================================================== l x l building blocks
+// (all called by the whole CTA, 256 threads; matrices in shared memory with ld kLD)
+
+// Fast fp64 1/sqrt(x) (x > 0) and 1/x (x != 0), finite normal operands: the fp64 MUFU
+// approximations (rsqrt/rcp.approx.ftz.f64, ~2^-22 relative) refined by two Newton steps to
+// ~1e-16 relative -- no fp32 conversions, ~3x shorter dependent chains than DSQRT / DDIV.
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
+// Blocked Cholesky A = R^T R of the symmetric l x l A (upper triangle read), R upper (zero below
+// the diagonal, identity beyond l), with 4 x 4 blocks on a 16 x 16 thread grid: thread (I, J)
+// keeps block A_IJ in registers.  Block step K: (a) thread (K, K) factors A_KK = R_KK^T R_KK;
+// (b) threads (K, J > K) form R_KJ = R_KK^{-T} A_KJ and publish row block K to R; (c) every
+// (I, J > K) applies A_IJ -= R_KI^T R_KJ.  Two barriers per 4 columns.  Returns false
+// (uniformly) on a pivot <= 1e-13 * max(diag) or a non-finite pivot.
+__device__ bool chol_upper(const double* A, double* R, double* flag, int l) {
+  const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
+  double a[4][4];
+  double dmax = 0.0;
+  for (int k = 0; k < l; ++k) dmax = fmax(dmax, A[k * kLD + k]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = 4 * bi + i, col = 4 * bj + j;
+      a[i][j] = (row < l && col < l) ? A[min(row, col) * kLD + max(row, col)] : (row == col ? 1.0 : 0.0);
+      if (row > col) R[row * kLD + col] = 0.0;
+    }
+  const double tol = 1e-13 * dmax;
+  if (tid == 0) flag[0] = 0.0;
+  const int nb = (l + 3) >> 2;
+  for (int K = 0; K < nb; ++K) {
+    if (bi == K && bj == K) {   // (a) 4 x 4 Cholesky in registers: a -> R_KK (upper)
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double piv = a[k][k];
+        if (!(piv > tol) || !(piv < DBL_MAX)) bad = true;
+        const double rs = bad ? 0.0 : rsqrt_fast(piv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[k][j] = j < k ? 0.0 : a[k][j] * rs;   // row k of R_KK
+#pragma unroll
+        for (int i = k + 1; i < 4; ++i)
+#pragma unroll
+          for (int j = i; j < 4; ++j) a[i][j] = fma(-a[k][i], a[k][j], a[i][j]);
+      }
+      if (bad) flag[0] = 1.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * K + j] = a[i][j];
+    }
+    __syncthreads();
+    if (flag[0] != 0.0) return false;
+    if (bi == K && bj > K) {    // (b) R_KJ = R_KK^{-T} A_KJ (forward substitution, 4 rows)
+      double rkk[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rkk[i][j] = R[(4 * K + i) * kLD + 4 * K + j];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double rinv = rcp_fast(rkk[k][k]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double v = a[k][j];
+#pragma unroll
+          for (int m = 0; m < k; ++m) v = fma(-rkk[m][k], a[m][j], v);
+          a[k][j] = v * rinv;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * bj + j] = a[i][j];
+    }
+    __syncthreads();
+    if (bi > K && bj >= bi) {   // (c) trailing update (upper blocks only)
+      double rki[4][4], rkj[4][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rki[m][i] = R[(4 * K + m) * kLD + 4 * bi + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rkj[m][j] = R[(4 * K + m) * kLD + 4 * bj + j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double v = a[i][j];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) v = fma(-rki[m][i], rkj[m][j], v);
+          a[i][j] = v;
+        }
+    }
+  }
+  for (int idx = tid; idx < (kSL - l) * kSL; idx += kST) {   // identity padding rows l..63
+    const int k = l + idx / kSL, j = idx % kSL;
+    R[k * kLD + j] = (k == j) ? 1.0 : 0.0;
+  }
+  for (int idx = tid; idx < l * (kSL - l); idx += kST) {     // zero padding columns of rows < l
+    const int k = idx / (kSL - l), j = l + idx % (kSL - l);
+    R[k * kLD + j] = 0.0;
+  }
+  __syncthreads();
+  return true;
+}
+
+// T = R^{-1} for the upper triangular R (identity beyond l), 4 x 4 blocks on the 16 x 16 thread
+// grid: diagonal blocks T_KK = R_KK^{-1} in parallel, then block super-diagonals d = 1..15:
+// T_IJ = -T_II sum_{K=I+1..J} R_IK T_KJ (one barrier per d).  T has leading dimension kMLD.
+__device__ void tri_inv_upper(const double* R, double* T, int l, double* /*unused*/) {
+  const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
+  const int nb = (l + 3) >> 2;
+  double tii[4][4];
+  {   // diagonal block of row block bi (every thread of row bi computes it: no exchange needed)
+    double r[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[i][j] = R[(4 * bi + i) * kLD + 4 * bi + j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tii[i][j] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {     // column c of the inverse: back substitution
+      tii[c][c] = rcp_fast(r[c][c]);
+#pragma unroll
+      for (int i = c - 1; i >= 0; --i) {
+        double v = 0.0;
+#pragma unroll
+        for (int m = i + 1; m <= c; ++m) v = fma(r[i][m], tii[m][c], v);
+        tii[i][c] = -v * rcp_fast(r[i][i]);
+      }
+    }
+  }
+  // every block of T: zero below the diagonal, T_II on it
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      T[(4 * bi + i) * kMLD + 4 * bj + j] = (bi == bj) ? tii[i][j] : 0.0;
+  __syncthreads();
+  for (int d = 1; d < nb; ++d) {
+    if (bj == bi + d) {
+      double sacc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[i][j] = 0.0;
+      for (int K = bi + 1; K <= bj; ++K) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          double rim[4], tmj[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rim[i] = R[(4 * bi + i) * kLD + 4 * K + m];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tmj[j] = T[(4 * K + m) * kMLD + 4 * bj + j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sacc[i][j] = fma(rim[i], tmj[j], sacc[i][j]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double v = 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) v = fma(tii[i][m], sacc[m][j], v);
+          T[(4 * bi + i) * kMLD + 4 * bj + j] = -v;
+        }
+    }
+    __syncthreads();
+  }
+}
+
+// Householder tridiagonalisation H^T A H = tridiag(d, e) of the symmetric l x l A (read only).
+// Thread (i = tid/4, part = tid%4) keeps A(i, part + 4jj), jj < 16, in registers.  The quad that
+// owns row k builds reflector k from its registers (quad shuffles only): v_k on rows k+1..l-1
+// with v_k(k+1) = x0 - alpha is stored in Hv row k, beta_k in hb[k].  Two barriers per reflector.
+__device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
+                        double* pvbuf, double* scal) {
+  const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
+  const unsigned qm = 0xFu << ((tid & 31) & ~3);
+  double w[16];
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    const int j = part + 4 * jj;
+    w[jj] = (i < l && j < l) ? A[min(i, j) * kLD + max(i, j)] : 0.0;
+  }
+  for (int k = 0; k + 2 < l; ++k) {
+    double* sc = scal + 2 * (k & 1);
+    if (i == k) {   // reflector k from row k (this quad's registers)
+      double ss = 0.0, x0 = 0.0, dk = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = part + 4 * jj;
+        if (j >= k + 2 && j < l) ss = fma(w[jj], w[jj], ss);
+        if (j == k + 1) x0 = w[jj];
+        if (j == k) dk = w[jj];
+      }
+      ss += __shfl_xor_sync(qm, ss, 1);
+      ss += __shfl_xor_sync(qm, ss, 2);
+      x0 += __shfl_xor_sync(qm, x0, 1);
+      x0 += __shfl_xor_sync(qm, x0, 2);
+      dk += __shfl_xor_sync(qm, dk, 1);
+      dk += __shfl_xor_sync(qm, dk, 2);
+      double beta = 0.0, alph = x0, v0 = 0.0;
+      if (ss > 0.0) {
+        const double t = ss + x0 * x0;
+        const double nrm = t * rsqrt_fast(t);
+        alph = x0 > 0.0 ? -nrm : nrm;
+        v0 = x0 - alph;
+        beta = 2.0 * rcp_fast(ss + v0 * v0);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = part + 4 * jj;
+        if (j > k && j < l) Hv[k * kLD + j] = (j == k + 1) ? v0 : w[jj];
+      }
+      if (part == 0) {
+        d[k] = dk;
+        e[k] = alph;
+        hb[k] = beta;
+        sc[0] = beta;
+      }
+    }
+    __syncthreads();
+    const double beta = sc[0];
+    const double* v = Hv + k * kLD;
+    if (beta != 0.0) {
+      // p_i = beta * sum_{j>k} A(i,j) v_j  for i > k; pv_i = p_i v_i
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; jj += 4) {
+        const int j = part + 4 * jj;
+        if (j > k && j < l) s0 = fma(w[jj], v[j], s0);
+        if (j + 4 > k && j + 4 < l) s1 = fma(w[jj + 1], v[j + 4], s1);
+        if (j + 8 > k && j + 8 < l) s2 = fma(w[jj + 2], v[j + 8], s2);
+        if (j + 12 > k && j + 12 < l) s3 = fma(w[jj + 3], v[j + 12], s3);
+      }
+      double s = (s0 + s1) + (s2 + s3);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (part == 0) {
+        const bool act = i > k && i < l;
+        pbuf[i] = act ? beta * s : 0.0;
+        pvbuf[i] = act ? beta * s * v[i] : 0.0;
+      }
+      __syncthreads();
+      // K = beta/2 p^T v (every thread, fixed order), w = p - K v, A -= v w^T + w v^T
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      for (int j = k + 1; j + 3 < l; j += 4) {
+        t0 += pvbuf[j];
+        t1 += pvbuf[j + 1];
+        t2 += pvbuf[j + 2];
+        t3 += pvbuf[j + 3];
+      }
+      for (int j = k + 1 + ((l - k - 1) & ~3); j < l; ++j) t0 += pvbuf[j];
+      const double K = 0.5 * beta * ((t0 + t1) + (t2 + t3));
+      if (i > k && i < l) {
+        const double vi = v[i], wi = pbuf[i] - K * vi;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = part + 4 * jj;
+          if (j > k && j < l) {
+            const double vj = v[j], wj = pbuf[j] - K * vj;
+            w[jj] -= fma(vi, wj, wi * vj);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // trailing 2 x 2 (or 1 x 1)
+  if (l >= 2) {
+    if (i == l - 2) {
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = part + 4 * jj;
+        if (j == l - 2) d[l - 2] = w[jj];
+        if (j == l - 1) e[l - 2] = w[jj];
+      }
+    }
+    if (i == l - 1) {
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+        if (part + 4 * jj == l - 1) d[l - 1] = w[jj];
+    }
+  } else if (i == 0 && part == 0) {
+    d[0] = w[0];
+  }
+  __syncthreads();
+}
+
+// Number of eigenvalues < mu of the symmetric tridiagonal (d, e2 = e^2): sign changes of the
+// Sturm sequence p_0 = 1, p_1 = d_0 - mu, p_k = (d_{k-1} - mu) p_{k-1} - e2_{k-2} p_{k-2},
+// rescaled by exact powers of two every 4 terms (|p| grows by at most ~||T||^4 in between);
+// an exact zero takes the sign opposite to its predecessor.
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int l, double mu) {
+  double pp = 1.0, p = d[0] - mu;
+  if (p == 0.0) p = -1e-300;
+  int cnt = (p < 0.0);
+  for (int k = 1; k < l; ++k) {
+    double pn = fma(d[k] - mu, p, -e2[k - 1] * pp);
+    if (pn == 0.0) pn = (p < 0.0) ? 1e-300 : -1e-300;
+    cnt += ((pn < 0.0) != (p < 0.0));
+    pp = p;
+    p = pn;
+    if ((k & 3) == 0) {
+      const int ex = max((int)((__double_as_longlong(p) >> 52) & 0x7ff), (int)((__double_as_longlong(pp) >> 52) & 0x7ff));
+      const double sc = __longlong_as_double((long long)(2046 - ex) << 52);   // 2^(1023-ex)
+      p *= sc;
+      pp *= sc;
+    }
+  }
+  return cnt;
+}
+
+// lambda_min of the tridiagonal by 256-point multisection: one log-spaced round over
+// [hi 2^-64, hi] (hi = min d_i >= lambda_min), then linear rounds to 1e-14 relative.
+__device__ double lambda_min_ms(const double* d, const double* e2, int l, int* ibuf, double* dbuf) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    double hi = d[0];
+    for (int k = 1; k < l; ++k) hi = fmin(hi, d[k]);
+    dbuf[0] = 0.0;
+    dbuf[1] = hi;
+  }
+  __syncthreads();
+  const double hi0 = dbuf[1];
+  if (!(hi0 > 0.0)) return 0.0;
+  for (int round = 0; round < 8; ++round) {
+    const double lo = dbuf[0], hi = dbuf[1];
+    if (round > 0 && hi - lo <= 1e-14 * hi) break;
+    auto point = [&](int t) -> double {   // t in [0, kST]: grid point t (t = kST -> hi)
+      if (round == 0) return t == 0 ? 0.0 : hi0 * exp2(-64.0 * (1.0 - (double)t / kST));
+      return lo + (hi - lo) * (double)t / kST;
+    };
+    if (tid == 0) ibuf[0] = kST;
+    __syncthreads();
+    if (sturm_count(d, e2, l, point(tid + 1)) > 0) atomicMin(ibuf, tid);
+    __syncthreads();
+    if (tid == 0) {
+      const int j = ibuf[0];   // smallest grid index whose point exceeds lambda_min
+      if (j < kST) {
+        dbuf[0] = point(j);
+        dbuf[1] = point(j + 1);
+      } else {
+        dbuf[0] = hi;          // lambda_min == hi (within rounding)
+        dbuf[1] = hi;
+      }
+    }
+    __syncthreads();
+  }
+  return 0.5 * (dbuf[0] + dbuf[1]);
+}
+
+// All l eigenvalues (ascending, lam[c] = c-th smallest) by Sturm bisection: one 256-point
+// log-spaced scan over the Gershgorin range, then 4 threads per eigenvalue, 5-section rounds.
+__device__ void all_eigs(const double* d, const double* e, const double* e2, int l, double* lam, double* blo,
+                         double* bhi, int* cnt) {
+  const int tid = threadIdx.x;
+  __shared__ double s_gl, s_gu;
+  if (tid == 0) {
+    double gl = DBL_MAX, gu = -DBL_MAX;
+    for (int k = 0; k < l; ++k) {
+      const double r = (k > 0 ? fabs(e[k - 1]) : 0.0) + (k + 1 < l ? fabs(e[k]) : 0.0);
+      gl = fmin(gl, d[k] - r);
+      gu = fmax(gu, d[k] + r);
+    }
+    const double nrm = fmax(fabs(gl), fabs(gu));
+    s_gl = gl - 1e-14 * nrm - 1e-300;
+    s_gu = gu + 1e-14 * nrm + 1e-300;
+  }
+  __syncthreads();
+  const double gl = s_gl, gu = s_gu;
+  // scan: point t = gu * 2^{-64 (1 - (t+1)/256)}, counts in cnt[t]
+  const double pt = gu * exp2(-64.0 * (1.0 - (double)(tid + 1) / kST));
+  cnt[tid] = (gu > 0.0) ? sturm_count(d, e2, l, pt) : l;
+  __syncthreads();
+  if (tid < l) {
+    // smallest scan point with count > c
+    int t = 0;
+    while (t < kST && cnt[t] <= tid) ++t;
+    double lo = (t == 0) ? gl : gu * exp2(-64.0 * (1.0 - (double)t / kST));
+    double hi = (t < kST) ? gu * exp2(-64.0 * (1.0 - (double)(t + 1) / kST)) : gu;
+    if (t == 0) lo = fmin(gl, 0.0);
+    blo[tid] = lo;
+    bhi[tid] = hi;
+  }
+  __syncthreads();
+  const int c = tid >> 2, part = tid & 3;
+  for (int round = 0; round < 40; ++round) {
+    double mu = 0.0;
+    int k = 0;
+    if (c < l) {
+      const double lo = blo[c], hi = bhi[c];
+      mu = lo + (hi - lo) * (double)(part + 1) / 5.0;
+      k = sturm_count(d, e2, l, mu);
+    }
+    cnt[tid] = k;
+    __syncthreads();
+    int done = 1;
+    if (c < l && part == 0) {
+      double lo = blo[c], hi = bhi[c];
+      const double base = lo;
+      const double w = hi - lo;
+      for (int s = 0; s < 4; ++s) {
+        const double m = base + w * (double)(s + 1) / 5.0;
+        if (cnt[4 * c + s] <= c) lo = fmax(lo, m);
+        else hi = fmin(hi, m);
+      }
+      blo[c] = lo;
+      bhi[c] = hi;
+      done = (hi - lo) <= 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300;
+    }
+    if (__syncthreads_and(done)) break;
+  }
+  if (tid < l) lam[tid] = 0.5 * (blo[tid] + bhi[tid]);
+  __syncthreads();
+}
+
+// Eigenvectors of the tridiagonal by inverse iteration (thread c < l: eigenvalue lam[c]); two
+// solves of (T - lam I) x = b with LU without pivoting (tiny pivots replaced by eps ||T||), a
+// deterministic start vector, normalised.  Z(i, c) = x_i.  LU pivots kept in Lu(i, c).
+__device__ void tri_eigvecs(const double* d, const double* e, const double* lam, int l, double* Z, double* Lu) {
+  const int c = threadIdx.x;
+  if (c < l) {
+    double tn = 0.0;
+    for (int k = 0; k < l; ++k)
+      tn = fmax(tn, fabs(d[k]) + (k > 0 ? fabs(e[k - 1]) : 0.0) + (k + 1 < l ? fabs(e[k]) : 0.0));
+    const double tiny = DBL_EPSILON * tn + 1e-300;
+    const double lm = lam[c];
+    for (int i = 0; i < l; ++i) {   // start vector: deterministic, no special structure
+      const uint32_t h = (uint32_t)(i * 0x9E3779B1u) ^ (uint32_t)(c * 0x85EBCA77u) ^ 0x2545F491u;
+      Z[i * kLD + c] = 0.5 + (double)((h >> 8) & 0xffff) * (1.0 / 65536.0);
+    }
+    for (int it = 0; it < 2; ++it) {
+      // forward: u_i = d_i - lam - m_i e_{i-1},  m_i = e_{i-1}/u_{i-1};  y_i = x_i - m_i y_{i-1}
+      double u = d[0] - lm;
+      if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+      Lu[c] = u;
+      double y = Z[c];
+      for (int i = 1; i < l; ++i) {
+        const double m = e[i - 1] / u;
+        u = d[i] - lm - m * e[i - 1];
+        if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+        Lu[i * kLD + c] = u;
+        y = Z[i * kLD + c] - m * y;
+        Z[i * kLD + c] = y;
+      }
+      // back: x_{l-1} = y_{l-1}/u_{l-1};  x_i = (y_i - e_i x_{i+1}) / u_i
+      double x = Z[(l - 1) * kLD + c] / Lu[(l - 1) * kLD + c];
+      Z[(l - 1) * kLD + c] = x;
+      double mx = fabs(x);
+      for (int i = l - 2; i >= 0; --i) {
+        x = (Z[i * kLD + c] - e[i] * x) / Lu[i * kLD + c];
+        Z[i * kLD + c] = x;
+        mx = fmax(mx, fabs(x));
+      }
+      // scale, then normalise
+      const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+      double s = 0.0;
+      for (int i = 0; i < l; ++i) {
+        const double v = Z[i * kLD + c] * inv;
+        Z[i * kLD + c] = v;
+        s += v * v;
+      }
+      const double rn = 1.0 / sqrt(s);
+      for (int i = 0; i < l; ++i) Z[i * kLD + c] *= rn;
+    }
+  }
+  __syncthreads();
+}
+
+// Z <- H_0 H_1 ... H_{l-3} Z  (H_k = I - beta_k v_k v_k^T on rows k+1..l-1), column-private quads.
+__device__ void back_transform(const double* Hv, const double* hb, int l, double* Z) {
+  const int tid = threadIdx.x, c = tid >> 2, part = tid & 3;
+  if (c < kSL) {
+    for (int k = l - 3; k >= 0; --k) {
+      const double b = hb[k];
+      double s = 0.0;
+      if (c < l && b != 0.0)
+        for (int j = k + 1 + part; j < l; j += 4) s += Hv[k * kLD + j] * Z[j * kLD + c];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (c < l && b != 0.0) {
+        const double f = b * s;
+        for (int j = k + 1 + part; j < l; j += 4) Z[j * kLD + c] -= f * Hv[k * kLD + j];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ============================================================== step kernel (cluster)
+struct StepArgs {
+  int n, l, r, step, q;
+  int shift, final_step;
+  int nblk;                 // Gram partial blocks of Y (reduce_gram_kernel)
+  const double* gpart;      // [nblk][np]
+  const double* Y;          // [l][n]
+  double* Q1;               // [l][n] scratch (two-pass)
+  double* g2part;           // [C][np]
+  double* gsum;             // [np] summed Gram of Y
+  double* amax;             // [C][2*64] (|value|, index) per column, final step
+  double* Qd;               // [l][n]
+  float* Qs;                // [l][n]
+  float* planes;            // [2 pN][pld] 3xTF32 planes of Q for the next op1 (nullptr: none)
+  int pN, pld;
+  double* alpha;
+  double* trace;            // [q]
+  double* sigma;            // [128]
+  int* status;              // [0] numeric, [1] fallback count, [2] q_used, [3] unused
+  float* U;                 // n x r (final step)
+  uint64_t seed;
+  uint32_t mode1;
+  double* dbg;              // optional phase clocks [mode][step][16]
+  int defer_alpha;          // non-final steps: the shift update runs in alpha_kernel (side stream)
+};
+
+struct StepSmem {
+  double G[kSL * kLD];      // Gram (later second-pass Gram); eigen path: Z aliases it
+  double R[kSL * kLD];      // Cholesky factor; eigen path: LU pivots
+  double T[kSL * kMLD];     // transform applied to the rows (ld kMLD)
+  double H[kSL * kLD];      // Householder vectors; product-chunk staging aliases it
+  double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL];
+  double xrow[kSL], pbuf[kSL], rowbuf[2 * kSL], scal[4], dbuf[4];
+  double colscale[kSL];
+  int valid[kSL];
+  int cnt[kST];
+  int ibuf[4];
+  int flags[4];
+};
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+// out(i, c) = sum_k X(i, k) M(k, c) for the nrow (<= 64) rows staged in Xs and c < l; thread
+// (rg = tid/16, cg = tid%16) computes rows 4rg.., columns 4cg.. in acc.  upper: M upper triangular.
+__device__ __forceinline__ void chunk_product(const double* Xs, const double* M, int l, bool upper,
+                                              double (&acc)[4][4]) {
+  const int tid = threadIdx.x, rg = tid >> 4, cgp = tid & 15;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  const int kend = upper ? min(l, 4 * cgp + 4) : l;
+#pragma unroll 2
+  for (int k = 0; k < kend; ++k) {
+    double x[4], m[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = Xs[(4 * rg + i) * kLD + k];
+    const double2 m01 = *reinterpret_cast<const double2*>(M + k * kMLD + 4 * cgp);
+    const double2 m23 = *reinterpret_cast<const double2*>(M + k * kMLD + 4 * cgp + 2);
+    m[0] = m01.x; m[1] = m01.y; m[2] = m23.x; m[3] = m23.y;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], m[j], acc[i][j]);
+  }
+}
+
+// Stage rows [i0, i0+nr) of the column-major X ([c][n]) into Xs (zero padded), via L2.
+__device__ void stage_rows(const double* X, int n, int l, int i0, int nr, double* Xs) {
+  constexpr int kPer = kChunk * kSL / kST;   // 16 loads per thread, all issued before use
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int idx = threadIdx.x + u * kST;
+    const int c = idx / kChunk, ii = idx % kChunk;
+    v[u] = (ii < nr && c < l) ? ldcg(X + (int64_t)c * n + i0 + ii) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int idx = threadIdx.x + u * kST;
+    const int c = idx / kChunk, ii = idx % kChunk;
+    Xs[ii * kLD + c] = v[u];
+  }
+  __syncthreads();
+}
+
+// Q rows [i0, i0+nr) staged in Xs -> fp64 master, fp32 shadow and (if planes) the 3xTF32 B
+// planes of the next op1 (hi = round-to-nearest tf32, lo = exact remainder), rows fastest.
+__device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, double* Qd, float* Qs,
+                              float* planes, int pN, int pld) {
+  const int cols = planes ? pN : l;
+  for (int idx = threadIdx.x; idx < cols * kChunk; idx += kST) {
+    const int c = idx / kChunk, row = idx % kChunk;
+    if (row < nr) {
+      const double v = c < l ? Xs[row * kLD + c] : 0.0;
+      const int64_t o = (int64_t)c * n + i0 + row;
+      const float f = (float)v;
+      if (c < l) {
+        Qd[o] = v;
+        Qs[o] = f;
+      }
+      if (planes) {
+        const float hi = sm100::tf32_rna(f);
+        planes[(int64_t)c * pld + i0 + row] = hi;
+        planes[(int64_t)(pN + c) * pld + i0 + row] = (float)(v - (double)hi);
+      }
+    }
+  }
+}
+
+// Fill G (symmetric, full) from packed upper entries in global memory (sum of `parts` arrays).
+__device__ void load_packed_sum(const double* src, int parts, int64_t stride, int l, double* G) {
+  const int np = l * (l + 1) / 2;
+  for (int e = threadIdx.x; e < np; e += kST) {
+    int c1, c2;
+    unpack_upper(e, c1, c2);
+    double s = 0.0;
+    for (int b = 0; b < parts; ++b) s += ldcg(src + (int64_t)b * stride + e);
+    G[c1 * kLD + c2] = s;
+    G[c2 * kLD + c1] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  StepSmem& S = *reinterpret_cast<StepSmem*>(smraw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int n = a.n, l = a.l;
+  const int np = l * (l + 1) / 2;
+  const int r0 = (int)((int64_t)rank * n / C), r1 = (int)((int64_t)(rank + 1) * n / C);
+  const double alpha0 = (a.step > 0) ? *a.alpha : 0.0;   // read before any cluster barrier
+  long long tck[16];
+  int ntck = 0;
+  tck[ntck++] = clock64();
+
+  // ---- 1. G = sum of the Gram partials (entries split across the cluster, fixed b order)
+  {
+    const int e0 = (int)((int64_t)rank * np / C), e1 = (int)((int64_t)(rank + 1) * np / C);
+    for (int e = e0 + tid; e < e1; e += kST) {
+      double s = 0.0;
+      int b = 0;
+      for (; b + 8 <= a.nblk; b += 8) {   // 8 independent loads in flight, summed in b order
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ldcg(a.gpart + (int64_t)(b + u) * np + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; b < a.nblk; ++b) s += ldcg(a.gpart + (int64_t)b * np + e);
+      a.gsum[e] = s;
+    }
+  }
+  tck[ntck++] = clock64();
+  cluster.sync();
+  load_packed_sum(a.gsum, 1, 0, l, S.G);
+  tck[ntck++] = clock64();
+
+  // ---- 2. the l x l factorisation (redundant in every CTA)
+  bool eig = a.final_step != 0;
+  bool two_pass = false;
+  double lam_min = 0.0, s1 = 0.0;
+  if (!eig) {
+    const bool ok = chol_upper(S.G, S.R, S.rowbuf, l);
+    if (!ok) {
+      eig = true;
+    } else {
+      tri_inv_upper(S.R, S.T, l, S.lam);
+      // kappa_F(R) = ||R||_F ||R^{-1}||_F >= kappa_2(Y); one CholQR pass leaves
+      // ||Q^T Q - I|| ~ eps kappa^2
+      if (tid < 32) {
+        double rf = 0.0, tf = 0.0;
+        for (int idx = tid; idx < l * l; idx += 32) {
+          const int i = idx / l, j = idx % l;
+          if (j >= i) {
+            rf += S.R[i * kLD + j] * S.R[i * kLD + j];
+            tf += S.T[i * kMLD + j] * S.T[i * kMLD + j];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          rf += __shfl_xor_sync(0xffffffffu, rf, o);
+          tf += __shfl_xor_sync(0xffffffffu, tf, o);
+        }
+        if (tid == 0) S.flags[0] = (DBL_EPSILON * rf * tf > 1e-10) ? 1 : 0;
+      }
+      __syncthreads();
+      two_pass = S.flags[0] != 0;
+      tck[ntck++] = clock64();
+      if (a.step > 0 && !a.defer_alpha) {
+        tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+        tck[ntck++] = clock64();
+        for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
+        __syncthreads();
+        lam_min = lambda_min_ms(S.d, S.e2, l, S.ibuf, S.dbuf);
+        if (tid == 0) {
+          double gmax = 0.0;   // sigma_1^2 >= max_i G_ii
+          for (int k = 0; k < l; ++k) gmax = fmax(gmax, S.G[k * kLD + k]);
+          S.dbuf[2] = sqrt(gmax);
+        }
+        __syncthreads();
+        s1 = S.dbuf[2];
+      }
+    }
+  }
+  if (eig) {
+    two_pass = true;
+    tck[ntck++] = clock64();
+    tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+    for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
+    __syncthreads();
+    tck[ntck++] = clock64();
+    all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+    tck[ntck++] = clock64();
+    double* Z = S.G;    // G no longer needed
+    tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R);
+    tck[ntck++] = clock64();
+    back_transform(S.H, S.hb, l, Z);
+    // T(:, cc) = V(:, l-1-cc) / sqrt(lambda): descending order; null columns flagged
+    const double sg1 = sqrt(fmax(S.lam[l - 1], 0.0));
+    if (tid == 0) S.flags[1] = 0;
+    __syncthreads();
+    for (int cc = tid; cc < l; cc += kST) {
+      const double sg = sqrt(fmax(S.lam[l - 1 - cc], 0.0));
+      const int ok = (sg > 1e-12 * sg1 && sg > 1e-200) ? 1 : 0;
+      S.valid[cc] = ok;
+      S.colscale[cc] = ok ? 1.0 / sg : 0.0;
+      if (!ok) atomicOr(&S.flags[1], 1);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kSL * kSL; idx += kST) {
+      const int k = idx / kSL, cc = idx % kSL;
+      S.T[k * kMLD + cc] = (k < l && cc < l) ? Z[k * kLD + (l - 1 - cc)] * S.colscale[cc] : 0.0;
+    }
+    __syncthreads();
+    lam_min = fmax(S.lam[0], 0.0);
+    s1 = sg1;
+  }
+
+  tck[ntck++] = clock64();
+  // ---- shift update (Alg. 3/4 lines 8-9) and reports: one writer
+  if (rank == 0 && tid == 0) {
+    const double sl = sqrt(fmax(lam_min, 0.0));
+    double a1 = alpha0;
+    if (a.step > 0 && a.shift && sl > alpha0 && !(sl < 1e-14 * s1)) a1 = 0.5 * (sl + alpha0);
+    if (a.step > 0 && !(a.defer_alpha && !a.final_step)) {
+      *a.alpha = a1;
+      a.trace[a.step - 1] = a1;
+      a.status[2] = a.step;
+    }
+    if (eig) {
+      int nf = 0;
+      for (int cc = 0; cc < l; ++cc) nf += S.valid[cc] ? 0 : 1;
+      a.status[1] += nf;
+    }
+    if (!(a.defer_alpha && !a.final_step)) a.sigma[126] = sl;
+  }
+  if (eig && a.final_step && rank == 0)
+    for (int cc = tid; cc < l; cc += kST) a.sigma[cc] = sqrt(fmax(S.lam[l - 1 - cc], 0.0)) + alpha0;
+
+  // ---- 3. rows of this CTA: Q = Y T (one pass) or Q1 = Y T, Gram2, Q = Q1 T2
+  double* Xs = S.H;   // staging (Householder vectors no longer needed)
+  const bool upperT = !eig;
+  double g2[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g2[i][j] = 0.0;
+  const int rg = tid >> 4, cgp = tid & 15;
+  for (int i0 = r0; i0 < r1; i0 += kChunk) {
+    const int nr = min(kChunk, r1 - i0);
+    stage_rows(a.Y, n, l, i0, nr, Xs);
+    if (i0 == r0) tck[ntck++] = clock64();
+    double acc[4][4];
+    chunk_product(Xs, S.T, l, upperT, acc);
+    __syncthreads();   // everyone done reading Xs
+    if (i0 == r0) tck[ntck++] = clock64();
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int row = 4 * rg + ii;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int c = 4 * cgp + jj;
+        double v = acc[ii][jj];
+        if (row >= nr || c >= l) v = 0.0;
+        Xs[row * kLD + c] = v;
+      }
+    }
+    __syncthreads();
+    if (eig && S.flags[1]) {
+      // rank-deficient columns (flagged invalid): deterministic Philox completion, which the
+      // second CholQR pass orthonormalises against the valid ones
+      for (int idx = tid; idx < nr * l; idx += kST) {
+        const int row = idx / l, c = idx % l;
+        if (!S.valid[c]) {
+          const uint4 x = omega_bits(a.seed ^ 0x5eed5eed5eed5eedull, 0x40000000u | (a.mode1 << 8) | (uint32_t)a.step,
+                                     (uint64_t)(i0 + row), (uint32_t)c);
+          const double v = (double)box_muller(x.x, x.y).x;
+          Xs[row * kLD + c] = v;
+          a.Q1[(int64_t)c * n + i0 + row] = v;
+        }
+      }
+      __syncthreads();
+    }
+    if (two_pass) {
+      for (int idx = tid; idx < l * kChunk; idx += kST) {   // coalesced: rows fastest
+        const int c = idx / kChunk, row = idx % kChunk;
+        if (row < nr) a.Q1[(int64_t)c * n + i0 + row] = Xs[row * kLD + c];
+      }
+    } else {
+      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld);
+    }
+    if (two_pass) {
+      // Gram2 partial (upper 4 x 4 blocks) of the Q1 rows now in Xs
+      if (cgp >= rg) {
+        for (int row = 0; row < nr; ++row) {
+          double x[4], y[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { x[i] = Xs[row * kLD + 4 * rg + i]; y[i] = Xs[row * kLD + 4 * cgp + i]; }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g2[i][j] = fma(x[i], y[j], g2[i][j]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  tck[ntck++] = clock64();
+  if (two_pass) {
+    // publish this CTA's Gram2 partial (packed upper), sum over the cluster
+    double* gp = a.g2part + (int64_t)rank * np;
+    if (cgp >= rg) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c1 = 4 * rg + i, c2 = 4 * cgp + j;
+          if (c1 <= c2 && c2 < l) gp[c2 * (c2 + 1) / 2 + c1] = g2[i][j];
+        }
+    }
+    cluster.sync();
+    load_packed_sum(a.g2part, C, np, l, S.G);
+    const bool ok2 = chol_upper(S.G, S.R, S.rowbuf, l);
+    if (!ok2) {
+      if (rank == 0 && tid == 0) a.status[0] = 6;   // RTK_ERR_NUMERIC
+      for (int idx = tid; idx < kSL * kSL; idx += kST) {
+        const int k = idx / kSL, c = idx % kSL;
+        S.T[k * kMLD + c] = (k == c) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+    } else {
+      tri_inv_upper(S.R, S.T, l, S.lam);
+    }
+    for (int i0 = r0; i0 < r1; i0 += kChunk) {
+      const int nr = min(kChunk, r1 - i0);
+      stage_rows(a.Q1, n, l, i0, nr, Xs);
+      double acc[4][4];
+      chunk_product(Xs, S.T, l, true, acc);
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int row = 4 * rg + ii;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int c = 4 * cgp + jj;
+          Xs[row * kLD + c] = (row < nr && c < l) ? acc[ii][jj] : 0.0;
+        }
+      }
+      __syncthreads();
+      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld);
+      __syncthreads();
+    }
+  }
+  tck[ntck++] = clock64();
+  if (rank == 0 && tid == 0 && a.dbg && a.step < 8 && a.mode1 <= 8) {
+    double* o = a.dbg + 16 * (a.mode1 - 1) * 8 + 16 * a.step;
+    o[0] = (double)ntck;
+    o[1] = eig ? 1.0 : 0.0;
+    o[2] = two_pass ? 1.0 : 0.0;
+    for (int z = 1; z < ntck && z < 14; ++z) o[2 + z] = (double)(tck[z] - tck[z - 1]);
+  }
+  // plane padding rows n..pld-1 (zero) -- the last CTA
+  if (a.planes && rank == C - 1) {
+    for (int idx = tid; idx < 2 * a.pN * (a.pld - n); idx += kST) {
+      const int c = idx / (a.pld - n), i = n + idx % (a.pld - n);
+      a.planes[(int64_t)c * a.pld + i] = 0.f;
+    }
+  }
+
+  // ---- 4. final step: U_k = Q(:, 1:r) with the sign pin (largest |entry| positive, lowest
+  // row index on ties), cluster-wide argmax
+  if (a.final_step) {
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int c = warp; c < a.r; c += kST / 32) {
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = r0 + lane; i < r1; i += 32) {
+        const double v = fabs(a.Qd[(int64_t)c * n + i]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        a.amax[(int64_t)rank * 2 * kSL + 2 * c] = best;
+        a.amax[(int64_t)rank * 2 * kSL + 2 * c + 1] = (double)bi;
+      }
+    }
+    cluster.sync();
+    for (int c = warp; c < a.r; c += kST / 32) {
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int b = 0; b < C; ++b) {
+        const double v = ldcg(a.amax + (int64_t)b * 2 * kSL + 2 * c);
+        const int iv = (int)ldcg(a.amax + (int64_t)b * 2 * kSL + 2 * c + 1);
+        if (v > best || (v == best && iv < bi)) { best = v; bi = iv; }
+      }
+      const double sgn = ldcg(a.Qd + (int64_t)c * n + bi) < 0.0 ? -1.0 : 1.0;
+      for (int i = r0 + lane; i < r1; i += 32) a.U[(int64_t)c * n + i] = (float)(sgn * a.Qd[(int64_t)c * n + i]);
+    }
+  }
+}
+
+// ============================================================== deferred shift update
+// Alg. 3/4 lines 8-9 for a non-final power step, off the critical path: the next power step's
+// streaming kernels need only Q, so this one-CTA kernel runs on a side stream concurrently with
+// them and is joined before the next reduce (which subtracts alpha Q).
+struct AlphaSmem {
+  double G[kSL * kLD];
+  double H[kSL * kLD];
+  double d[kSL], e[kSL], e2[kSL], hb[kSL], pbuf[kSL], pvbuf[kSL], scal[4], dbuf[4];
+  int ibuf[4];
+};
+
+__global__ void __launch_bounds__(kST, 1) alpha_kernel(const double* __restrict__ gsum, int l, int step, int shift,
+                                                      double* __restrict__ alpha, double* __restrict__ trace,
+                                                      int* __restrict__ status, double* __restrict__ sigma) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  AlphaSmem& S = *reinterpret_cast<AlphaSmem*>(smraw);
+  const int tid = threadIdx.x;
+  const double alpha0 = *alpha;
+  load_packed_sum(gsum, 1, 0, l, S.G);
+  tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.pvbuf, S.scal);
+  for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
+  __syncthreads();
+  const double lam_min = lambda_min_ms(S.d, S.e2, l, S.ibuf, S.dbuf);
+  if (tid == 0) {
+    double gmax = 0.0;   // sigma_1^2 >= max_i G_ii
+    for (int k = 0; k < l; ++k) gmax = fmax(gmax, S.G[k * kLD + k]);
+    const double s1 = sqrt(gmax);
+    const double sl = sqrt(fmax(lam_min, 0.0));
+    double a1 = alpha0;
+    if (shift && sl > alpha0 && !(sl < 1e-14 * s1)) a1 = 0.5 * (sl + alpha0);
+    *alpha = a1;
+    trace[step - 1] = a1;
+    status[2] = step;
+    sigma[126] = sl;
+  }
+}
+
+cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t st) {
+  const size_t smem = sizeof(AlphaSmem);
+  cudaError_t e = cudaFuncSetAttribute(alpha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  alpha_kernel<<<1, kST, smem, st>>>(B.gsum, B.l, step, shift ? 1 : 0, B.alpha, B.trace, B.status, B.sigma);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- host side
+double* g_step_dbg = nullptr;   // diagnostics: set by rtk_debug_clocks (not part of the product path)
+
+int solve_cluster_size(int n) {
+  int C = (n + 127) / 128;
+  return std::max(1, std::min(kMaxC, C));
+}
+
+size_t solve_gpart_doubles(int n, int l) { return (size_t)((n + kRBr - 1) / kRBr) * l * (l + 1) / 2; }
+
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st) {
+  const int nblk = (B.n + kRBr - 1) / kRBr;
+  reduce_gram_kernel<<<nblk, kST, 0, st>>>(B.Ypart, B.G, B.ltot, B.n_rows, B.n, B.l, B.Qd, B.alpha, power ? 1 : 0,
+                                           B.Y, B.gpart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
+                        float* planes, int pN, int pld, bool defer_alpha, cudaStream_t st) {
+  StepArgs a;
+  a.n = B.n; a.l = B.l; a.r = B.r; a.step = step; a.q = q;
+  a.shift = shift ? 1 : 0; a.final_step = (step == q) ? 1 : 0;
+  a.nblk = (B.n + kRBr - 1) / kRBr;
+  a.gpart = B.gpart; a.Y = B.Y; a.Q1 = B.Q1; a.g2part = B.g2part; a.gsum = B.gsum; a.amax = B.amax;
+  a.Qd = B.Qd; a.Qs = B.Qs; a.planes = planes; a.pN = pN; a.pld = pld;
+  a.alpha = B.alpha; a.trace = B.trace; a.sigma = B.sigma; a.status = B.status;
+  a.U = U; a.seed = seed; a.mode1 = mode1;
+  a.dbg = g_step_dbg;
+  a.defer_alpha = defer_alpha ? 1 : 0;
+  const int C = solve_cluster_size(B.n);
+  const size_t smem = sizeof(StepSmem);
+  cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(kST, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, step_kernel, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace rtk

@@ -490,7 +490,7 @@ cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* p
 
 // op1: W planes (or shrink output) from the column-major M (view v) and B planes (ld round4(n))
 cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,
-                   int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st) {
+                   int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st, int max_ctas) {
   const int N = tc_npad(l);
   CUtensorMap mM, mB;
   const int ldp = (v.n + 3) / 4 * 4;
@@ -499,7 +499,7 @@ cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t 
   TcOp1Args a;
   a.n = v.n; a.N = N; a.l = l; a.m = v.m(); a.nk = (v.n + kBK - 1) / kBK; a.ntiles = (v.m() + 127) / 128;
   a.W = W; a.ldw = ldw; a.shrink = shrink ? 1 : 0; a.out = out; a.Rprev = Rprev; a.nnext = nnext; a.ldnext = ldnext;
-  const int grid = (int)std::min<int64_t>(num_sms(), a.ntiles);
+  const int grid = (int)std::min<int64_t>(max_ctas > 0 ? max_ctas : num_sms(), a.ntiles);
   switch (N) {
     case 16: return op1_launch<16>(mM, mB, a, grid, st);
     case 32: return op1_launch<32>(mM, mB, a, grid, st);
