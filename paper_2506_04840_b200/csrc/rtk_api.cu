@@ -287,6 +287,8 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   const uint32_t mode1 = (uint32_t)(k + 1);
   const bool tc = L.tc_range[k] && tc_supported(v, l);
   Side* side = nullptr;
+  const char* fz = getenv("RTK_FUSED");
+  const bool fused = tc && fast && !(fz && fz[0] == '0') && fused_supported(v, l);   // single-pass power step
   const bool defer = fast && tc && P.q > 1;   // deferred shift updates on the side stream
   if (defer) RTK_CK(side_streams(&side));
   bool pending = false;                       // an alpha_kernel is in flight on side->aux
@@ -297,6 +299,13 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       float* planes = (float*)(ws + L.planes);
       float* W = (float*)(ws + L.wbuf);
       const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
+      if (fused && step > 0) {   // (the sketch keeps tc_op2: its in-kernel Omega generation is faster)
+        int Gf = 0, rows = 0;
+        RTK_CK(fused_power(v, l, planes, (int)pad4(n), step == 0, seed, mode1, B.Ypart,
+                           pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st));
+        g_launches += 1;
+        B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
+      } else {
       if (step == 0) {
         RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G, st));
         g_launches += 1;
@@ -307,6 +316,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         g_launches += 3;
       }
       B.G = G; B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
+      }
     } else {
     TileLaunch T;
     T.v = v;

@@ -111,4 +111,11 @@ cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t 
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
                    float* Ypart, int G, cudaStream_t st);
 
+// ---- fused single-pass power step (rtk_fused.cu) -----------------------------------
+int fused_cluster(int n);
+bool fused_supported(const View& v, int l);
+size_t fused_ypart_floats(const View& v, int l, int grid);
+cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
+                        uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st);
+
 }  // namespace rtk
