@@ -389,6 +389,16 @@ int run_shrink(const Problem& P, const Layout& L, char* ws, int k, const View& v
   else { T.nnext = 1; T.ldnext = 1; }
   T.out = out;
   ProfScope ps(2, k, st);
+  const char* fz = getenv("RTK_FUSED");
+  if (L.tc_shrink[k] && tc_supported(v, P.ranks[k]) && !(fz && fz[0] == '0') && fused_supported(v, P.ranks[k])) {
+    float* planes = (float*)(ws + L.planes);
+    RTK_CK(tc_split(nullptr, Uk, v.n, P.ranks[k], planes, st));
+    int Gf = 0, rows = 0;
+    RTK_CK(fused_power(v, P.ranks[k], planes, (int)pad4(v.n), false, 0, 0, nullptr, num_sms(), &Gf, &rows, st, out,
+                       T.Rprev, T.nnext, T.ldnext));
+    g_launches += 2;
+    return RTK_OK;
+  }
   if (L.tc_shrink[k] && tc_supported(v, P.ranks[k])) {
     float* planes = (float*)(ws + L.planes);
     RTK_CK(tc_split(nullptr, Uk, v.n, P.ranks[k], planes, st));

@@ -116,6 +116,7 @@ int fused_cluster(int n);
 bool fused_supported(const View& v, int l);
 size_t fused_ypart_floats(const View& v, int l, int grid);
 cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
-                        uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st);
+                        uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st,
+                        float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1);
 
 }  // namespace rtk
