@@ -233,7 +233,9 @@ def run_ours(args, ws, rank, local):
     ms_step = max_over_ranks(ms_local, ws)
     value = ms_step / ws
 
-    # ---- roofline of the dominant kernel: fused power step on mode 1 ----
+    # ---- roofline of the dominant kernel: the fused 3xTF32 power step on mode 1 ----
+    # algorithmic work per launch (one power step): the unfolding read once,
+    # 4 n m bytes, and Y = M (M^T Q): 4 n m l flops, executed as 3 tf32 tensor products each
     n, m, l = dims[0], 1, ranks[0] + p
     for j in dims[1:]:
         m *= j
@@ -242,8 +244,12 @@ def run_ours(args, ws, rank, local):
     flops = 4.0 * n * m * l
     bytes_alg = 4.0 * n * m
     peaks, src = load_peaks()
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = nsm * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    hbm_peak = peaks["hbm_gbs"]
+    bf16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+    tf32_peak = bf16 / 2.0      # dense tf32 = bf16 / 2 (B200_PROFILING.md nominal ratio), sustained
+    t_hbm = bytes_alg / (hbm_peak * 1e9)
+    t_tc = 3.0 * flops / (tf32_peak * 1e12)
+    bound = "tensor" if t_tc >= t_hbm else "hbm"
     tot_ms = sum(prof.ms[k][j] for k in range(4) for j in range(8))
     share = prof.ms[1][0] / tot_ms if tot_ms > 0 else None
     traffic = None
@@ -253,18 +259,25 @@ def run_ours(args, ws, rank, local):
             traffic = json.load(open(tf)).get("power_step_mode1_dram_bytes")
         except Exception:
             traffic = None
-    roof = {"bound": "alu", "achieved": flops / t_pow / 1e12 if t_pow > 0 else None,
-            "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": (flops / t_pow / 1e12) / fp32_peak if t_pow > 0 else None,
+    if bound == "tensor":
+        achieved = 3.0 * flops / t_pow / 1e12 if t_pow > 0 else None
+        peak, unit = tf32_peak, "TFLOP/s"
+    else:
+        achieved = bytes_alg / t_pow / 1e9 if t_pow > 0 else None
+        peak, unit = hbm_peak, "GB/s"
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if achieved else None,
             "traffic": traffic,
-            "kernel": f"tile_kernel<POWER> mode 1 (n={n}, m={m}, l={l}), FP32 FFMA",
-            "peak_src": f"FP32 FFMA {nsm} SMs x 128 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0):g} MHz "
-                        f"(sm_max_mhz from MEASURED_PEAKS.json, {src})",
+            "kernel": f"fused_power_kernel mode 1 (n={n}, m={m}, l={l}): single HBM pass, 3xTF32 tcgen05",
+            "algorithmic": {"bytes": bytes_alg, "flops_fp32": flops, "tf32_flops_3x": 3.0 * flops},
+            "peak_src": (f"tf32 dense = {bf16:g}/2 TFLOP/s (bf16 sustained from MEASURED_PEAKS.json, {src}); "
+                         f"HBM {hbm_peak:g} GB/s"),
+            "roofline_ms": max(t_hbm, t_tc) * 1e3,
             "launch_ms": t_pow * 1e3, "launches_timed": cnt,
             "share_of_step": share,
             "hbm_achieved_gbs": bytes_alg / t_pow / 1e9 if t_pow > 0 else None,
-            "hbm_frac": (bytes_alg / t_pow / 1e9) / peaks["hbm_gbs"] if t_pow > 0 else None,
-            "hbm_peak_gbs": peaks["hbm_gbs"]}
+            "hbm_frac": (bytes_alg / t_pow / 1e9) / hbm_peak if t_pow > 0 else None,
+            "hbm_peak_gbs": hbm_peak}
     breakdown = {k: round(sum(prof.ms[i][j] for j in range(8)) / args.steps, 4)
                  for i, k in enumerate(["sketch", "power", "shrink", "small_solves"])}
 
