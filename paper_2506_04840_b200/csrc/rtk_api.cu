@@ -550,6 +550,22 @@ int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float
   View v;
   v.base = M; v.n = (int)n; v.P = 1; v.S = m; v.sp = 1; v.si = 1; v.ss = ld;
   const char* pe = getenv("RTK_PATH");
+  const char* fz = getenv("RTK_FUSED");
+  if (!(pe && std::string(pe) == "ffma") && tc_supported(v, l) && !(fz && fz[0] == '0') && fused_supported(v, l)) {
+    // the fused single-pass engine of the solver (rtk_fused.cu)
+    const int N = tc_npad(l), G = num_sms();
+    const int64_t pld = pad4(n);
+    float *planes = nullptr, *yp = nullptr;
+    RTK_CK(cudaMallocAsync((void**)&planes, (size_t)2 * N * pld * 4, st));
+    RTK_CK(cudaMallocAsync((void**)&yp, fused_ypart_floats(v, l, G) * 4, st));
+    RTK_CK(tc_split(nullptr, Q, (int)n, l, planes, st));
+    int Gf = 0, rows = 0;
+    RTK_CK(fused_power(v, l, planes, (int)pld, false, 0, 0, yp, G, &Gf, &rows, st));
+    RTK_CK(launch_sum_partials(yp, Gf, N, rows, (int)n, l, Y, st));
+    RTK_CK(cudaFreeAsync(planes, st));
+    RTK_CK(cudaFreeAsync(yp, st));
+    return RTK_OK;
+  }
   if (!(pe && std::string(pe) == "ffma") && tc_supported(v, l)) {
     const int N = tc_npad(l), nit = (int)((n + 127) / 128), G = num_sms();
     const int64_t ldw = pad4(m);

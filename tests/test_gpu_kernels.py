@@ -47,18 +47,22 @@ def test_omega_bit_exact_config_shapes(cfg):
 #  tc    : 3xTF32 (hi*hi + hi*lo + lo*hi, the lo plane of the streamed operand itself rounded
 #          to tf32: ~2^-21 per product) with the tensor core's fp32 accumulation over K = n
 #          (op1) and K = m / #CTAs (op2): bound 4e-5 (measured <= 1.6e-5 at n=1000, m=2e5).
-TOL = {"ffma": 2e-6, "tc": 4e-5}
+#  fused: the solver's single-pass engine (rtk_fused.cu): the same 3xTF32 products with the
+#          streamed operand split in registers (exact lo) and W summed over the 2-CTA row split.
+TOL = {"ffma": 2e-6, "tc": 4e-5, "fused": 4e-5}
 
 
-@pytest.mark.parametrize("path", ["ffma", "tc"])
+@pytest.mark.parametrize("path", ["ffma", "tc", "fused"])
 @pytest.mark.parametrize("n,m,l", [(1, 7, 1), (3, 50, 2), (64, 4096, 10), (80, 1000, 15),
                                    (200, 3000, 30), (400, 2001, 40), (1000, 1234, 60),
                                    (37, 333, 13), (1500, 700, 20), (4096, 100, 8), (130, 5000, 64),
-                                   (1000, 200000, 60), (256, 129, 48)])
+                                   (1000, 200000, 60), (256, 129, 48), (513, 777, 17), (600, 3000, 48),
+                                   (1024, 4099, 33)])
 def test_power_step_vs_fp64(n, m, l, path, monkeypatch):
     torch = cuda_or_skip()
     from paper_2506_04840_b200 import power_step
-    monkeypatch.setenv("RTK_PATH", path)
+    monkeypatch.setenv("RTK_PATH", "ffma" if path == "ffma" else "tc")
+    monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
     rng = np.random.default_rng(n * 7 + m)
     M = rng.standard_normal((n, m)).astype(np.float32)
     Q = np.linalg.qr(rng.standard_normal((n, l)))[0].astype(np.float32)

@@ -50,10 +50,11 @@ def check(a, ranks, p, q, seed, sequential, gaps=None, alpha_rtol=1e-3):
     return re_g, re_o
 
 
-@pytest.mark.parametrize("path", ["ffma", "tc"])
+@pytest.mark.parametrize("path", ["ffma", "tc", "fused"])
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4"])
 def test_config_parity(cfg, path, monkeypatch):
-    monkeypatch.setenv("RTK_PATH", path)
+    monkeypatch.setenv("RTK_PATH", "ffma" if path == "ffma" else "tc")
+    monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
     c = CONFIGS[cfg]
     a = make_config_tensor(cfg)
     check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], c["algo"] == "rsthosvd")
@@ -61,6 +62,8 @@ def test_config_parity(cfg, path, monkeypatch):
 
 @pytest.mark.parametrize("seq", [False, True])
 @pytest.mark.parametrize("dims,ranks,p,q", [
+    ((640, 40, 36), (20, 8, 6), 6, 3),        # n_1 > 512: fused engine on a 2-CTA row split
+    ((1000, 30, 20), (30, 6, 5), 10, 2),      # n_1 = 1000 (the C5 mode-1 row count), l = 40
     ((40, 30), (6, 4), 2, 2),                 # d = 2, the matrix case
     ((37, 29, 23), (4, 5, 3), 3, 2),          # odd sizes: scalar loader, ragged tiles
     ((16, 12, 10, 9), (3, 2, 4, 2), 2, 3),    # d = 4
