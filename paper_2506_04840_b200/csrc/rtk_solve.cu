@@ -310,20 +310,23 @@ __device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* 
   for (int k = 0; k + 2 < l; ++k) {
     double* sc = scal + 2 * (k & 1);
     if (i == k) {   // reflector k from row k (this quad's registers)
-      double ss = 0.0, x0 = 0.0, dk = 0.0;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0}, x0 = 0.0, dk = 0.0;
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
         const int j = part + 4 * jj;
-        if (j >= k + 2 && j < l) ss = fma(w[jj], w[jj], ss);
+        if (j >= k + 2 && j < l) s4[jj & 3] = fma(w[jj], w[jj], s4[jj & 3]);
         if (j == k + 1) x0 = w[jj];
         if (j == k) dk = w[jj];
       }
-      ss += __shfl_xor_sync(qm, ss, 1);
-      ss += __shfl_xor_sync(qm, ss, 2);
-      x0 += __shfl_xor_sync(qm, x0, 1);
-      x0 += __shfl_xor_sync(qm, x0, 2);
-      dk += __shfl_xor_sync(qm, dk, 1);
-      dk += __shfl_xor_sync(qm, dk, 2);
+      // quad sums through shared memory (partial-mask shuffles in a divergent warp are slow)
+      double* qs = scal + 4 + 12 * (k & 1);   // [3][4]
+      qs[part] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      qs[4 + part] = x0;
+      qs[8 + part] = dk;
+      __syncwarp(qm);
+      double ss = (qs[0] + qs[1]) + (qs[2] + qs[3]);
+      x0 = (qs[4] + qs[5]) + (qs[6] + qs[7]);
+      dk = (qs[8] + qs[9]) + (qs[10] + qs[11]);
       double beta = 0.0, alph = x0, v0 = 0.0;
       if (ss > 0.0) {
         const double t = ss + x0 * x0;
@@ -367,16 +370,13 @@ __device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* 
         pvbuf[i] = act ? beta * s * v[i] : 0.0;
       }
       __syncthreads();
-      // K = beta/2 p^T v (every thread, fixed order), w = p - K v, A -= v w^T + w v^T
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-      for (int j = k + 1; j + 3 < l; j += 4) {
-        t0 += pvbuf[j];
-        t1 += pvbuf[j + 1];
-        t2 += pvbuf[j + 2];
-        t3 += pvbuf[j + 3];
-      }
-      for (int j = k + 1 + ((l - k - 1) & ~3); j < l; ++j) t0 += pvbuf[j];
-      const double K = 0.5 * beta * ((t0 + t1) + (t2 + t3));
+      // K = beta/2 p^T v (every warp, same fixed order: lanes j and j+32, then a butterfly),
+      // w = p - K v, A -= v w^T + w v^T
+      const int lane = tid & 31;
+      double t0 = pvbuf[lane] + pvbuf[lane + 32];   // pvbuf is zero outside (k, l)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+      const double K = 0.5 * beta * t0;
       if (i > k && i < l) {
         const double vi = v[i], wi = pbuf[i] - K * vi;
 #pragma unroll
@@ -645,7 +645,7 @@ struct StepSmem {
   double T[kSL * kMLD];     // transform applied to the rows (ld kMLD)
   double H[kSL * kLD];      // Householder vectors; product-chunk staging aliases it
   double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL];
-  double xrow[kSL], pbuf[kSL], rowbuf[2 * kSL], scal[4], dbuf[4];
+  double xrow[kSL], pbuf[kSL], rowbuf[2 * kSL], scal[32], dbuf[4];
   double colscale[kSL];
   int valid[kSL];
   int cnt[kST];
@@ -1051,7 +1051,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
 struct AlphaSmem {
   double G[kSL * kLD];
   double H[kSL * kLD];
-  double d[kSL], e[kSL], e2[kSL], hb[kSL], pbuf[kSL], pvbuf[kSL], scal[4], dbuf[4];
+  double d[kSL], e[kSL], e2[kSL], hb[kSL], pbuf[kSL], pvbuf[kSL], scal[32], dbuf[4];
   int ibuf[4];
 };
 
