@@ -299,10 +299,14 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       float* planes = (float*)(ws + L.planes);
       float* W = (float*)(ws + L.wbuf);
       const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
-      if (fused && step > 0) {   // (the sketch keeps tc_op2: its in-kernel Omega generation is faster)
+      // sketch on the fused engine only for long unfoldings (Omega-plane generation has a fixed
+      // cost; tc_op2 generates Omega in shared memory and is faster for small m)
+      if (fused && (step > 0 || v.m() >= 200000)) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
         int Gf = 0, rows = 0;
-        RTK_CK(fused_power(v, l, planes, (int)pad4(n), step == 0, seed, mode1, B.Ypart,
+        const bool sk = step == 0;
+        RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
                            pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st));
+        g_launches += sk ? 1 : 0;
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
       } else {
