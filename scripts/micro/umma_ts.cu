@@ -94,7 +94,19 @@ __global__ void __launch_bounds__(128, 1) ts_kernel(const float* A, const float*
     const uint64_t ad = sdesc_sw128(smem_addr(sm + 32768), 16, 1024);
     umma_ts(tb, tb + acol, bd, IDESC, 0);   // D = A B^T once (checked below)
     t0 = clock64();
-    if (ts) {
+    if (ts == 2) {
+      // the fused kernel's stage: A hi/lo at TMEM cols 384 + 8 k8 (+32), B hi/lo planes at +0/+8 KB
+      const uint64_t bd_lo = sdesc_sw128(smem_addr(sm + 8192), 16, 1024);
+      for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k8 = 0; k8 < 4; ++k8) {
+          const uint32_t ahi = tb + 384 + 8 * k8, alo = ahi + 32;
+          umma_ts(tb + 128, alo, bd + 2 * k8, IDESC, 1);
+          umma_ts(tb + 128, ahi, bd_lo + 2 * k8, IDESC, 1);
+          umma_ts(tb + 128, ahi, bd + 2 * k8, IDESC, 1);
+        }
+      }
+    } else if (ts) {
       for (int i = 0; i < iters; ++i) {
 #pragma unroll
         for (int k = 0; k < 12; ++k) umma_ts(tb + 128, tb + acol, bd, IDESC, 1);
@@ -160,11 +172,11 @@ void run() {
   unsigned long long c[148];
   const int iters = 2000;
   for (int hm = 0; hm <= 2; ++hm)
-  for (int ts = 0; ts <= 1; ++ts) {
+  for (int ts = 0; ts <= 2; ++ts) {
     ts_kernel<N><<<148, 128, smem>>>(dA, dB, dD, iters, ts, dc, hm);
     cudaDeviceSynchronize();
     cudaMemcpy(c, dc, 148 * 8, cudaMemcpyDeviceToHost);
-    printf("N=%3d %s hammer=%s: %.2f cyc/mma   layout max err %.3e (|D| %.2f) [%s]\n", N, ts ? "A in TMEM" : "A in SMEM",
+    printf("N=%3d %s hammer=%s: %.2f cyc/mma   layout max err %.3e (|D| %.2f) [%s]\n", N, ts == 2 ? "stage pattern (TMEM A)" : ts ? "A in TMEM" : "A in SMEM",
            hm == 0 ? "none" : hm == 1 ? "tmem-st" : "lds", (double)c[1 % 148] / (iters * 12), err, nrm, cudaGetErrorString(cudaGetLastError()));
   }
 }
