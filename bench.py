@@ -105,13 +105,22 @@ def barrier(ws):
 
 
 def max_over_ranks(x: float, ws: int) -> float:
+    """Max of a per-rank device time over the job (NCCL on GPUs, gloo on CPU)."""
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def job_value(ms_local: float, ws: int):
+    """(ms_per_step, value): the step time is the max over ranks; the job solves ws independent
+    replicas in that time, so the job's ms per solve is ms_step / ws (scaling "weak")."""
+    ms_step = max_over_ranks(ms_local, ws)
+    return ms_step, ms_step / ws
 
 
 def cfg_block(cfg_name, c):
@@ -230,8 +239,7 @@ def run_ours(args, ws, rank, local):
     prof = rt.profile_end()
     clocks = clk.stop()
     ms_local = e0.elapsed_time(e1) / args.steps
-    ms_step = max_over_ranks(ms_local, ws)
-    value = ms_step / ws
+    ms_step, value = job_value(ms_local, ws)
 
     # ---- roofline of the dominant kernel: the fused 3xTF32 power step on mode 1 ----
     # algorithmic work per launch (one power step): the unfolding read once,
