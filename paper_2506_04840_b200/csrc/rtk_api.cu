@@ -348,10 +348,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       }
       RTK_CK(launch_reduce_gram2(B, step > 0, st));
       const bool dstep = defer && step > 0 && step < P.q;
-      RTK_CK(launch_step(B, step, P.q, shift, step == P.q ? Uk : nullptr, seed, mode1, planes, tc_npad(l),
-                         (int)pad4(n), dstep, st));
-      g_launches += 2;
-      if (dstep) {
+      if (dstep) {   // the shift update reads the reduce's Gram partials: it runs beside step_kernel
         RTK_CK(cudaEventRecord(side->ev_step, st));
         RTK_CK(cudaStreamWaitEvent(side->aux, side->ev_step, 0));
         RTK_CK(launch_alpha(B, step, shift, side->aux));
@@ -359,6 +356,9 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         pending = true;
         g_launches += 1;
       }
+      RTK_CK(launch_step(B, step, P.q, shift, step == P.q ? Uk : nullptr, seed, mode1, planes, tc_npad(l),
+                         (int)pad4(n), dstep, st));
+      g_launches += 2;
     } else {
       ProfScope ps(3, k, st);
       RTK_CK(launch_reduce_gram(B, step > 0, st));

@@ -1055,14 +1055,34 @@ struct AlphaSmem {
   int ibuf[4];
 };
 
-__global__ void __launch_bounds__(kST, 1) alpha_kernel(const double* __restrict__ gsum, int l, int step, int shift,
+__global__ void __launch_bounds__(kST, 1) alpha_kernel(const double* __restrict__ gpart, int nblk, int l, int step,
+                                                      int shift,
                                                       double* __restrict__ alpha, double* __restrict__ trace,
                                                       int* __restrict__ status, double* __restrict__ sigma) {
   extern __shared__ __align__(16) uint8_t smraw[];
   AlphaSmem& S = *reinterpret_cast<AlphaSmem*>(smraw);
   const int tid = threadIdx.x;
   const double alpha0 = *alpha;
-  load_packed_sum(gsum, 1, 0, l, S.G);
+  {   // G = sum_b Gram_b in the same fixed b order as step_kernel (identical G, identical alpha)
+    const int np = l * (l + 1) / 2;
+    for (int e = tid; e < np; e += kST) {
+      double sum = 0.0;
+      int b = 0;
+      for (; b + 8 <= nblk; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(gpart + (int64_t)(b + u) * np + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
+      }
+      for (; b < nblk; ++b) sum += __ldcg(gpart + (int64_t)b * np + e);
+      int c1, c2;
+      unpack_upper(e, c1, c2);
+      S.G[c1 * kLD + c2] = sum;
+      S.G[c2 * kLD + c1] = sum;
+    }
+    __syncthreads();
+  }
   tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.pvbuf, S.scal);
   for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
   __syncthreads();
@@ -1085,7 +1105,8 @@ cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t s
   const size_t smem = sizeof(AlphaSmem);
   cudaError_t e = cudaFuncSetAttribute(alpha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  alpha_kernel<<<1, kST, smem, st>>>(B.gsum, B.l, step, shift ? 1 : 0, B.alpha, B.trace, B.status, B.sigma);
+  alpha_kernel<<<1, kST, smem, st>>>(B.gpart, (B.n + kRBr - 1) / kRBr, B.l, step, shift ? 1 : 0, B.alpha, B.trace,
+                                     B.status, B.sigma);
   return cudaGetLastError();
 }
 
