@@ -73,8 +73,12 @@ typedef struct rtk_report {
 typedef struct rtk_options {
   int32_t sequential; /* 0: T-HOSVD (Alg. 3, every mode factors A_(k)); 1: ST-HOSVD (Alg. 4) */
   int32_t shift;      /* 1: adaptive shift (Alg. 3/4); 0: alpha == 0 (Alg. 2)                */
-  double pve_tol;     /* > 0: Alg. B.1 PVE stop per mode with q as q_max (ST only)           */
-  int32_t path;       /* 0: auto, 1: FP32 FFMA tiles (other values reserved)                 */
+  double pve_tol;     /* > 0: Alg. B.1 per mode, q is q_max: after power
+                       * step j, sigma = diag(Sigma)+alpha; stop (U_k = that step's basis, no
+                       * shift update) when max_{i<=r_k}|sigma_i - sigmahat_i| <= pve_tol *
+                       * sigma_{r_k+1}.  RTK_ERR_ARG unless sequential, p >= 1, r_k+p <= 64.
+                       * q_used / alpha_trace report the steps taken (trace zero past them). */
+  int32_t path;       /* 0: auto, 1: FP32 FFMA tiles, 2: tcgen05 3xTF32 (RTK_ERR_SHAPE if n/a)  */
 } rtk_options;
 
 /*

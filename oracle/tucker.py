@@ -114,6 +114,8 @@ def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
     """
     n, cols = m.shape
     l = r + p
+    if pve_tol is not None and p < 1:
+        raise ValueError("Alg. B.1 compares against sigma_{r+1}: needs p >= 1")
     om = omega(seed, mode1, 0, cols, l).astype(np.float64)    # line 3: Omega_k
     q_mat, _ = econ_svd(m @ om)                                 # line 5
     alpha = 0.0                                                 # line 5: alpha = 0
@@ -165,7 +167,9 @@ def rsthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True
              pve=None) -> Result:
     """Alg. 4, shifted randomized ST-HOSVD, order (1..d).
 
-    shift=False is Alg. 2's ST branch; pve=(tol, q_max) is Alg. B.1.
+    shift=False is Alg. 2's ST branch; pve=(tol, q_max) is Alg. B.1 (pinned by
+    tests/test_oracle_tucker.py::test_pve_*: reductions to Alg. 4 at q_max and q = 1, the
+    rank-l closed form sigma = lambda_i(M M^T), monotonicity in tol).
     G starts as A; mode k factors G_(k) then G = G x_k U_k^T (line 12).
     """
     g = np.asarray(a, dtype=np.float64)

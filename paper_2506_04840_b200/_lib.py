@@ -171,8 +171,11 @@ _WS = _WorkspaceCache()
 
 
 def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: bool = True,
-          report: bool = False, out=None, workspace=None):
+          report: bool = False, out=None, workspace=None, pve_tol: float = 0.0, path: int = 0):
     """General solver: Alg. 4 (sequential) / Alg. 3 (not sequential); shift=False is Alg. 2.
+
+    pve_tol > 0 selects Alg. B.1 (PAPER.md:1145-1172) with q as q_max (sequential only);
+    path: 0 auto, 1 FP32 FFMA tiles, 2 tcgen05 3xTF32 (rtk_options.path).
 
     Returns (core, [U_1..U_d]) or (core, U, Report) with report=True.
     ``out=(core, [U_k])`` reuses caller-allocated outputs (column-major).
@@ -201,7 +204,7 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
     ws_bytes = workspace_bytes(sequential, dims, ranks, p, q) if min(ranks) >= 1 else 0
     ws = workspace if workspace is not None else _WS.get(dev, max(ws_bytes, 1))
-    opt = _Options(1 if sequential else 0, 1 if shift else 0, 0.0, 0)
+    opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path))
     rep = None
     bufs = None
     if report:
@@ -225,7 +228,7 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     r_obj = Report([list(at[k * q:(k + 1) * q]) for k in range(d)],
                    [list(sg[k * 128:k * 128 + ls[k]]) for k in range(d)],
                    list(qu), rep.fallback, rep.numeric,
-                   [[sg[k * 128 + 100 + s] for s in range(q + 1)] for k in range(d)])
+                   [[sg[k * 128 + 100 + s] for s in range(min(q + 1, 24))] for k in range(d)])
     return core, U, r_obj
 
 

@@ -71,6 +71,7 @@ struct Problem {
   std::vector<int> ranks;
   int p = 0, q = 0;
   bool seq = true;
+  double pve = 0.0;   // > 0: Alg. B.1 tolerance, q is q_max
 };
 
 // m_k: columns of the matrix mode k factors (PAPER.md:257 vs :300)
@@ -289,7 +290,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   Side* side = nullptr;
   const char* fz = getenv("RTK_FUSED");
   const bool fused = tc && fast && !(fz && fz[0] == '0') && fused_supported(v, l);   // single-pass power step
-  const bool defer = fast && tc && P.q > 1;   // deferred shift updates on the side stream
+  const bool pve = P.pve > 0.0;   // Alg. B.1: the step kernel decides the stop, alpha inline
+  const int* stop = pve ? B.status + 3 : nullptr;
+  if (pve) RTK_CK(cudaMemsetAsync(B.sighat, 0, (size_t)l * sizeof(double), st));   // sigmahat = 0
+  const bool defer = fast && tc && P.q > 1 && !pve;   // deferred shift updates on the side stream
   if (defer) RTK_CK(side_streams(&side));
   bool pending = false;                       // an alpha_kernel is in flight on side->aux
   for (int step = 0; step <= P.q; ++step) {
@@ -305,7 +309,8 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         int Gf = 0, rows = 0;
         const bool sk = step == 0;
         RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
-                           pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st));
+                           pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st, nullptr, 1, 1,
+                           1, sk ? nullptr : stop));
         g_launches += sk ? 1 : 0;
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
@@ -346,7 +351,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         RTK_CK(cudaStreamWaitEvent(st, side->ev_alpha, 0));
         pending = false;
       }
-      RTK_CK(launch_reduce_gram2(B, step > 0, st));
+      RTK_CK(launch_reduce_gram2(B, step > 0, st, step > 0 ? stop : nullptr));
       const bool dstep = defer && step > 0 && step < P.q;
       if (dstep) {   // the shift update reads the reduce's Gram partials: it runs beside step_kernel
         RTK_CK(cudaEventRecord(side->ev_step, st));
@@ -356,8 +361,9 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         pending = true;
         g_launches += 1;
       }
-      RTK_CK(launch_step(B, step, P.q, shift, step == P.q ? Uk : nullptr, seed, mode1, planes, tc_npad(l),
-                         (int)pad4(n), dstep, st));
+      // B.1 may stop at any power step: U_k is written by the step that stops (or the last)
+      RTK_CK(launch_step(B, step, P.q, shift, (step == P.q || (pve && step > 0)) ? Uk : nullptr, seed, mode1,
+                         planes, tc_npad(l), (int)pad4(n), dstep, pve ? P.pve : 0.0, st));
       g_launches += 2;
     } else {
       ProfScope ps(3, k, st);
@@ -429,7 +435,14 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   int rc = validate(P);
   if (rc) return rc;
   if ((uintptr_t)A % 4) return fail(RTK_ERR_ALIGN, "A must be 4-byte aligned");
-  if (opt.pve_tol > 0.0) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) is not implemented on the GPU path yet");
+  if (opt.pve_tol > 0.0) {   // Alg. B.1 is stated for Alg. 4
+    if (!P.seq) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) applies to the sequential algorithm (Alg. 4) only");
+    if (p < 1) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) needs p >= 1 (it compares against sigma_{r+1})");
+    if (q < 1) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) needs q_max >= 1");
+    for (int k = 0; k < d; ++k)
+      if (ranks[k] + p > kSolveLMax) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) needs r_k + p <= 64");
+    P.pve = opt.pve_tol;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (opt.path < 0 || opt.path > 2) return fail(RTK_ERR_ARG, "path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
   const Layout L = plan(P, num_sms(), A, opt.path);

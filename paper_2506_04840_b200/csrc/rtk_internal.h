@@ -97,9 +97,9 @@ int num_sms();
 constexpr int kSolveLMax = 64;
 extern double* g_step_dbg;
 size_t solve_gpart_doubles(int n, int l);      // Gram partials of reduce_gram_kernel
-cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st);
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop = nullptr);
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
-                        float* planes, int pN, int pld, bool defer_alpha, cudaStream_t st);
+                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st);
 cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t st);
 
 // ---- tcgen05 3xTF32 path (rtk_tc.cu) -------------------------------------------
@@ -117,6 +117,7 @@ bool fused_supported(const View& v, int l);
 size_t fused_ypart_floats(const View& v, int l, int grid);
 cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
                         uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st,
-                        float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1);
+                        float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1,
+                        const int* stop = nullptr);
 
 }  // namespace rtk

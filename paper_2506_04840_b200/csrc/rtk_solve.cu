@@ -61,8 +61,10 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
                                                          int n_rows, int n, int l,
                                                          const double* __restrict__ Qd,
                                                          const double* __restrict__ alpha, int power,
-                                                         double* __restrict__ Y, double* __restrict__ gpart) {
+                                                         double* __restrict__ Y, double* __restrict__ gpart,
+                                                         const int* __restrict__ stop) {
   __shared__ double Ys[kRBr][kSL + 1];
+  if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kRBr;
   const int rows = min(kRBr, n - i0);
@@ -631,12 +633,14 @@ struct StepArgs {
   double* alpha;
   double* trace;            // [q]
   double* sigma;            // [128]
-  int* status;              // [0] numeric, [1] fallback count, [2] q_used, [3] unused
+  int* status;              // [0] numeric, [1] fallback count, [2] q_used, [3] B.1 stopped
   float* U;                 // n x r (final step)
   uint64_t seed;
   uint32_t mode1;
   double* dbg;              // optional phase clocks [mode][step][16]
   int defer_alpha;          // non-final steps: the shift update runs in alpha_kernel (side stream)
+  double pve_tol;           // > 0: Alg. B.1 stopping rule on power steps
+  double* sighat;           // [kSL] B.1 sigma-hat of the previous power step (zero at mode start)
 };
 
 struct StepSmem {
@@ -647,6 +651,7 @@ struct StepSmem {
   double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL];
   double xrow[kSL], pbuf[kSL], rowbuf[2 * kSL], scal[32], dbuf[4];
   double colscale[kSL];
+  double shat[kSL];         // B.1 sigma-hat, read before the first cluster barrier
   int valid[kSL];
   int cnt[kST];
   int ibuf[4];
@@ -748,6 +753,11 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   const int np = l * (l + 1) / 2;
   const int r0 = (int)((int64_t)rank * n / C), r1 = (int)((int64_t)(rank + 1) * n / C);
   const double alpha0 = (a.step > 0) ? *a.alpha : 0.0;   // read before any cluster barrier
+  const bool pve = a.pve_tol > 0.0 && a.step > 0;
+  // Alg. B.1 stopped this mode at an earlier power step: the remaining launches are no-ops
+  if (pve && *(volatile const int*)(a.status + 3)) return;
+  if (pve)
+    for (int i = tid; i < kSL; i += kST) S.shat[i] = i < l ? a.sighat[i] : 0.0;
   long long tck[16];
   int ntck = 0;
   tck[ntck++] = clock64();
@@ -774,10 +784,36 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   load_packed_sum(a.gsum, 1, 0, l, S.G);
   tck[ntck++] = clock64();
 
-  // ---- 2. the l x l factorisation (redundant in every CTA)
-  bool eig = a.final_step != 0;
-  bool two_pass = false;
+  // ---- 2a. Alg. B.1 lines 9-12: all eigenvalues of G = Y^T Y give
+  // Sigma = sqrt(lambda) (descending); sigma = Sigma + alpha; stop when
+  // max_{i<=r} |sigma_i - sigmahat_i| <= tol * sigma_{r+1}.  Identical in every CTA.
+  bool stop = false, have_eigs = false;
   double lam_min = 0.0, s1 = 0.0;
+  if (pve) {
+    tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+    for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
+    __syncthreads();
+    all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+    if (tid == 0) {
+      double dmax = 0.0;
+      for (int i = 0; i < a.r; ++i)
+        dmax = fmax(dmax, fabs(sqrt(fmax(S.lam[l - 1 - i], 0.0)) + alpha0 - S.shat[i]));
+      const double sr = sqrt(fmax(S.lam[l - 1 - a.r], 0.0)) + alpha0;
+      S.flags[2] = (dmax <= a.pve_tol * sr) ? 1 : 0;
+    }
+    __syncthreads();
+    stop = S.flags[2] != 0;
+    have_eigs = true;
+    lam_min = fmax(S.lam[0], 0.0);
+    s1 = sqrt(fmax(S.lam[l - 1], 0.0));
+    // line 15: sigmahat = sigma (every CTA copied sigmahat before the first cluster barrier)
+    if (!stop && rank == 0)
+      for (int i = tid; i < l; i += kST) a.sighat[i] = sqrt(fmax(S.lam[l - 1 - i], 0.0)) + alpha0;
+  }
+
+  // ---- 2. the l x l factorisation (redundant in every CTA)
+  bool eig = a.final_step != 0 || stop;
+  bool two_pass = false;
   if (!eig) {
     const bool ok = chol_upper(S.G, S.R, S.rowbuf, l);
     if (!ok) {
@@ -805,7 +841,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       __syncthreads();
       two_pass = S.flags[0] != 0;
       tck[ntck++] = clock64();
-      if (a.step > 0 && !a.defer_alpha) {
+      if (a.step > 0 && !a.defer_alpha && !have_eigs) {
         tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
         tck[ntck++] = clock64();
         for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
@@ -824,11 +860,13 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   if (eig) {
     two_pass = true;
     tck[ntck++] = clock64();
-    tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
-    for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
-    __syncthreads();
-    tck[ntck++] = clock64();
-    all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+    if (!have_eigs) {   // tridiag / all_eigs results are still intact when B.1 computed them
+      tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+      for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
+      __syncthreads();
+      tck[ntck++] = clock64();
+      all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+    }
     tck[ntck++] = clock64();
     double* Z = S.G;    // G no longer needed
     tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R);
@@ -840,7 +878,10 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     __syncthreads();
     for (int cc = tid; cc < l; cc += kST) {
       const double sg = sqrt(fmax(S.lam[l - 1 - cc], 0.0));
-      const int ok = (sg > 1e-12 * sg1 && sg > 1e-200) ? 1 : 0;
+      // Gram eigenvalues below l eps lambda_max are zero to working accuracy (the Gram squares
+      // the condition of Y, whose fp32-accumulated entries carry ~1e-7 relative noise anyway);
+      // their inverse-iteration vectors are not orthogonal: those columns are completed instead
+      const int ok = (S.lam[l - 1 - cc] > kSL * DBL_EPSILON * S.lam[l - 1] && sg > 1e-200) ? 1 : 0;
       S.valid[cc] = ok;
       S.colscale[cc] = ok ? 1.0 / sg : 0.0;
       if (!ok) atomicOr(&S.flags[1], 1);
@@ -861,11 +902,13 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     const double sl = sqrt(fmax(lam_min, 0.0));
     double a1 = alpha0;
     if (a.step > 0 && a.shift && sl > alpha0 && !(sl < 1e-14 * s1)) a1 = 0.5 * (sl + alpha0);
+    if (stop) a1 = alpha0;   // B.1 line 11: break before the shift update
     if (a.step > 0 && !(a.defer_alpha && !a.final_step)) {
       *a.alpha = a1;
       a.trace[a.step - 1] = a1;
       a.status[2] = a.step;
     }
+    if (stop) a.status[3] = 1;
     if (eig) {
       int nf = 0;
       for (int cc = 0; cc < l; ++cc) nf += S.valid[cc] ? 0 : 1;
@@ -873,7 +916,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     }
     if (!(a.defer_alpha && !a.final_step)) a.sigma[126] = sl;
   }
-  if (eig && a.final_step && rank == 0)
+  if (eig && (a.final_step || stop) && rank == 0)
     for (int cc = tid; cc < l; cc += kST) a.sigma[cc] = sqrt(fmax(S.lam[l - 1 - cc], 0.0)) + alpha0;
 
   // ---- 3. rows of this CTA: Q = Y T (one pass) or Q1 = Y T, Gram2, Q = Q1 T2
@@ -1008,7 +1051,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
 
   // ---- 4. final step: U_k = Q(:, 1:r) with the sign pin (largest |entry| positive, lowest
   // row index on ties), cluster-wide argmax
-  if (a.final_step) {
+  if (a.final_step || stop) {
     __syncthreads();
     const int warp = tid >> 5, lane = tid & 31;
     for (int c = warp; c < a.r; c += kST / 32) {
@@ -1120,15 +1163,15 @@ int solve_cluster_size(int n) {
 
 size_t solve_gpart_doubles(int n, int l) { return (size_t)((n + kRBr - 1) / kRBr) * l * (l + 1) / 2; }
 
-cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st) {
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop) {
   const int nblk = (B.n + kRBr - 1) / kRBr;
   reduce_gram_kernel<<<nblk, kST, 0, st>>>(B.Ypart, B.G, B.ltot, B.n_rows, B.n, B.l, B.Qd, B.alpha, power ? 1 : 0,
-                                           B.Y, B.gpart);
+                                           B.Y, B.gpart, stop);
   return cudaGetLastError();
 }
 
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
-                        float* planes, int pN, int pld, bool defer_alpha, cudaStream_t st) {
+                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st) {
   StepArgs a;
   a.n = B.n; a.l = B.l; a.r = B.r; a.step = step; a.q = q;
   a.shift = shift ? 1 : 0; a.final_step = (step == q) ? 1 : 0;
@@ -1139,6 +1182,8 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   a.U = U; a.seed = seed; a.mode1 = mode1;
   a.dbg = g_step_dbg;
   a.defer_alpha = defer_alpha ? 1 : 0;
+  a.pve_tol = pve_tol;
+  a.sighat = B.sighat;
   const int C = solve_cluster_size(B.n);
   const size_t smem = sizeof(StepSmem);
   cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -249,3 +249,120 @@ def test_config_c1_oracle_ballpark():
     re_det = metrics.relative_error(a, det_core, det_us)
     assert abs(re - re_det) <= 1e-6 * re_det
     assert 0.02 < re < 0.08
+
+
+# ------------------------------------------------------------ Alg. B.1 (PVE)
+# Pins for tucker._range_finder(pve_tol=...) / rsthosvd(pve=...).
+def _decaying_tensor(seed, dims=(24, 20, 18), decay=0.35):
+    rng = np.random.default_rng(seed)
+    core = rng.standard_normal(dims) * np.exp(-decay * np.indices(dims).sum(axis=0))
+    return tucker_tensor(core, [orthonormal_factor(n, n, rng) for n in dims], dtype=np.float64)
+
+
+def test_pve_tiny_tol_is_algorithm_4_at_q_max():
+    """No stop (tol -> 0) runs q_max steps of Alg. 4 (B.1 line 6 loop = Alg. 4 line 6)."""
+    a = _decaying_tensor(31)
+    full = tucker.rsthosvd(a, (4, 3, 5), p=3, q=5, seed=9)
+    pve = tucker.rsthosvd(a, (4, 3, 5), p=3, q=0, seed=9, pve=(1e-300, 5))
+    for t_f, t_p in zip(full.traces, pve.traces):
+        assert t_p.q == 5 and t_p.alpha == t_f.alpha
+    for u_f, u_p in zip(full.factors, pve.factors):
+        np.testing.assert_array_equal(u_f, u_p)
+    np.testing.assert_array_equal(full.core, pve.core)
+
+
+def test_pve_huge_tol_stops_after_first_step():
+    """sigmahat = 0 at j = 1, so max_i sigma_i = sigma_1 <= tol sigma_{r+1} stops there with
+    U_k from that step (B.1 lines 9-12) and no shift update: equals Alg. 4 with q = 1."""
+    a = _decaying_tensor(32)
+    one = tucker.rsthosvd(a, (4, 3, 5), p=3, q=1, seed=9)
+    pve = tucker.rsthosvd(a, (4, 3, 5), p=3, q=0, seed=9, pve=(1e12, 6))
+    for t in pve.traces:
+        assert t.q == 1 and t.alpha == [0.0]
+    for u_1, u_p in zip(one.factors, pve.factors):
+        np.testing.assert_array_equal(u_1, u_p)
+    np.testing.assert_array_equal(one.core, pve.core)
+
+
+def test_pve_closed_form_rank_l_matrix():
+    """rank(M) = l: the sketch spans range(M) exactly, so Sigma_j = lambda_i - alpha_{j-1} and
+    sigma = Sigma + alpha = lambda_i(M M^T) at every step (PAPER.md:272-286 with B.1 line 9).
+    Step 1 compares against sigmahat = 0: it stops iff lambda_1 <= tol lambda_{r+1} (the
+    (r+1)-th value, 1-based), else step 2 sees sigma == sigmahat and stops for any tol > 0."""
+    rng = np.random.default_rng(33)
+    n, m, r, p = 18, 40, 3, 2
+    l = r + p
+    sv = np.array([9.0, 5.0, 3.0, 2.0, 1.5])
+    mm = orthonormal_factor(n, l, rng) @ np.diag(sv) @ orthonormal_factor(m, l, rng).T
+    lam = sv ** 2                                   # eigenvalues of M M^T, descending
+    ratio = lam[0] / lam[r]                         # sigma_1 / sigma_{r+1} at step 1
+    for tol, q_exp in [(1e-9, 2), (0.5 * ratio, 2), (ratio * (1 - 1e-9), 2), (ratio * (1 + 1e-9), 1)]:
+        _, tr = tucker._range_finder(mm, r, p, q=0, seed=5, mode1=1, shift=True, pve_tol=(tol, 8))
+        assert tr.q == q_exp, (tol, tr.q)
+        np.testing.assert_allclose(tr.sigma[0][:l] + 0.0, lam, rtol=1e-12)   # alpha_0 = 0
+        if q_exp == 2:
+            # step 2 stops before the shift update: alpha stays lambda_l / 2 (closed form above)
+            assert len(tr.alpha) == 2 and tr.alpha[0] == tr.alpha[1]
+            assert abs(tr.alpha[1] - lam[l - 1] / 2) <= 1e-12 * lam[0]
+            np.testing.assert_allclose(tr.sigma[1][:l] + tr.alpha[0], lam, rtol=1e-12)
+
+
+def test_pve_monotone_in_tol():
+    """The iterates do not depend on tol until the stop, so a larger tol never stops later."""
+    for s in range(8):
+        rng = np.random.default_rng(200 + s)
+        n, m = int(rng.integers(12, 30)), int(rng.integers(30, 80))
+        sv = np.exp(-rng.uniform(0.02, 0.3) * np.arange(n))
+        mm = orthonormal_factor(n, n, rng) @ np.diag(sv) @ orthonormal_factor(m, n, rng).T
+        qs = []
+        for tol in [1e-8, 1e-6, 1e-4, 1e-3, 1e-2, 1e-1, 1.0, 10.0]:
+            _, tr = tucker._range_finder(mm, 3, 3, q=0, seed=s, mode1=1, shift=True, pve_tol=(tol, 12))
+            assert 1 <= tr.q <= 12 and len(tr.alpha) == tr.q
+            qs.append(tr.q)
+        assert all(b <= a for a, b in zip(qs, qs[1:])), qs
+
+
+def test_pve_needs_sigma_r_plus_1():
+    """B.1 compares against sigma_{r_k+1}: p = 0 leaves it undefined (rejected)."""
+    with pytest.raises(ValueError):
+        tucker._range_finder(np.eye(6), 2, 0, q=0, seed=1, mode1=1, shift=True, pve_tol=(0.1, 3))
+
+
+def _table_b1_rows():
+    import os
+    rows = []
+    path = os.path.join(os.path.dirname(__file__), "golden", "table_b1_tensor_b.txt")
+    for line in open(path):
+        if line.strip() and not line.startswith("#"):
+            kind, r, tol, q1, q2, q3, re = line.split()
+            rows.append((kind, int(r), float(tol), (int(q1), int(q2), int(q3)), float(re)))
+    return rows
+
+
+def test_table_b1_tensor_b_re_is_the_optimum():
+    """Tensor B is orthogonally decomposable, so the best rank-(r,r,r)
+    Tucker error is sqrt(sum_{i>r} v_i^2 / sum v_i^2); every Table B.1 row read into
+    tests/golden/ prints that value to its 3 digits (the PVE runs converged)."""
+    from workloads import tensor_b_spectrum
+    rows = _table_b1_rows()
+    assert len(rows) == 16
+    for kind, r, tol, qs, re in rows:
+        v = tensor_b_spectrum(600, kind)
+        cf = np.sqrt(np.sum(v[r:] ** 2) / np.sum(v ** 2))
+        assert float(f"{cf:.2e}") == re, (kind, r, tol, cf, re)
+
+
+@pytest.mark.parametrize("kind", ["slow", "fast"])
+def test_pve_tensor_b_reaches_closed_form(kind):
+    """Alg. B.1 on a 60^3 tensor B: RE >= the closed-form optimum and within 1e-3 of it
+    for loose and tight tol (the stop rule never ends before the leading sigmas settle)."""
+    from workloads import make_tensor_b, tensor_b_spectrum
+    a = make_tensor_b(60, kind, 7).astype(np.float64)
+    v = tensor_b_spectrum(60, kind)
+    for r in (8, 15):
+        cf = np.sqrt(np.sum(v[r:] ** 2) / np.sum(v ** 2))
+        for tol in (0.5, 0.01):
+            res = tucker.rsthosvd(a, (r, r, r), 5, 0, 3, pve=(tol, 30))
+            re = metrics.relative_error(a, res.core, res.factors)
+            assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (kind, r, tol, re, cf)
+            assert all(2 <= t.q <= 30 for t in res.traces)

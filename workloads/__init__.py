@@ -170,3 +170,42 @@ def make_config_tensor_torch(name: str, device="cuda"):
                                                      dtype=torch.float64)
         out_rev.view(nd, slab_elems)[s0:s1] = slab.to(torch.float32)
     return out_rev.permute(*reversed(range(d)))        # shape dims, column-major strides
+
+
+# ---------------------------------------------------------------- tensor B
+def tensor_b_spectrum(n: int, kind: str) -> np.ndarray:
+    """v of tensor B, i = 1..n: slow 1/i^2, fast exp(-i/7),
+    sshape 0.001 + 1/(1 + exp(i - 29))."""
+    i = np.arange(1, n + 1, dtype=np.float64)
+    if kind == "slow":
+        return 1.0 / i ** 2
+    if kind == "fast":
+        return np.exp(-i / 7.0)
+    if kind == "sshape":
+        return 0.001 + 1.0 / (1.0 + np.exp(i - 29.0))
+    raise ValueError(kind)
+
+
+def make_tensor_b(n: int, kind: str, seed: int, d: int = 3) -> np.ndarray:
+    """B = tendiag(v, [n]*d) x_1 A_1 ... x_d A_d with A_k = orth(N(0,1)^{n x n})
+    (PAPER.md:806-810); host build for small n (float32, Fortran order)."""
+    rng = np.random.default_rng(seed)
+    v = tensor_b_spectrum(n, kind)
+    core = np.zeros((n,) * d)
+    core[(np.arange(n),) * d] = v
+    return tucker_tensor(core, [orthonormal_factor(n, n, rng) for _ in range(d)])
+
+
+def make_tensor_b_torch(n: int, kind: str, seed: int, device="cuda"):
+    """Tensor B (d = 3) built on ``device`` in float64 (the paper's 600^3 size), returned as
+    a column-major float32 tensor: B = sum_i v_i a1_i o a2_i o a3_i."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    v = torch.as_tensor(tensor_b_spectrum(n, kind), device=device)
+    fac = [torch.linalg.qr(torch.randn((n, n), generator=g, device=device, dtype=torch.float64))[0]
+           for _ in range(3)]
+    # column-major (a fastest): store as [c][b][a]
+    ab = torch.einsum("ai,bi->bai", fac[0] * v, fac[1]).reshape(n * n, n)    # [(b,a)][i]
+    out = (fac[2] @ ab.T).to(torch.float32)                                    # [c][(b,a)]
+    return out.reshape(n, n, n).permute(2, 1, 0)
