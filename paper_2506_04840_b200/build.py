@@ -16,6 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
          "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-diag-suppress", "550"]
+# diagnostics only, e.g. RTK_EXTRA_NVCC_FLAGS=-DRTK_FUSED_PROF=1 (fused-kernel role timers)
+FLAGS += os.environ.get("RTK_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:
