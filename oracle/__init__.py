@@ -17,7 +17,7 @@ gauss   Philox4x32-10 + RTK-GAUSS-1 Box-Muller (the Omega_k of Alg. 3/4,
 tucker  unfold / fold / mode-k product, Alg. 1
         (PAPER.md:113-125), Alg. 2 (PAPER.md:211-237), Alg. 3
         (PAPER.md:250-270), Alg. 4 (PAPER.md:293-313), Alg. B.1
-        (PAPER.md:1145-1172).
+        (PAPER.md:1145-1172), Alg. A.2 / A.1 (PAPER.md:1094-1116, :1072-1091).
 metrics RE, principal angles, spectral gaps,
         orthonormality.
 

@@ -103,14 +103,15 @@ class Result:
 
 
 def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
-                  shift: bool, pve_tol=None):
+                  shift: bool, pve_tol=None, full: bool = False):
     """Lines 3-13 of Alg. 3 / Alg. 4 for one mode.
 
     m      : the matrix being factored, A_(k) (Alg. 3) or G_(k) (Alg. 4), float64
     mode1  : 1-based mode index (Philox counter word, DESIGN.md RTK-GAUSS-1)
     shift  : False -> Alg. 2 (alpha fixed at 0)
     pve_tol: (tol, q_max) -> Alg. B.1 stopping rule
-    Returns (U_k sign-pinned n x r, ModeTrace).
+    full   : return the whole n x l basis Q_k of the last iterate (Alg. A.2 line 12), unpinned
+    Returns (U_k sign-pinned n x r, ModeTrace), or (Q_k n x l, ModeTrace) with full=True.
     """
     n, cols = m.shape
     l = r + p
@@ -141,6 +142,8 @@ def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
         tr.alpha.append(alpha)
         if pve_tol is not None:
             sig_hat = sig                                       # B.1 line 15
+    if full:
+        return q_mat, tr
     u = sign_pin(q_mat[:, :r])                                   # line 12: Q(:,1:r_k)
     return u, tr
 
@@ -179,4 +182,36 @@ def rsthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True
         us.append(u)
         trs.append(tr)
         g = mode_product(g, u.T, k)
+    return Result(g, us, trs)
+
+
+def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True) -> Result:
+    """Alg. A.2, holistic shifted randomized ST-HOSVD; shift=False is
+    Alg. A.1.  Order 1..d.
+
+    Lines 2-13: B = A; mode k runs the shifted range finder of Alg. 4 on B_(k) with
+    l_k = r_k + p columns and keeps ALL l_k columns: B = B x_k Q_k^T (so mode k+1 sees
+    l_1..l_k, n_{k+1}..n_d; Omega_k has l_1..l_{k-1} n_{k+1}..n_d rows, line 3).
+    Line 14: deterministic ST-HOSVD of the l_1 x ... x l_d tensor B (Alg. 1, ST branch):
+    V_k = first r_k left singular vectors of G_(k), G = G x_k V_k^T.
+    Line 15: U_k = Q_k V_k, sign-pinned (C6); V_k's columns carry the same signs so that the
+    core stays G = A x_1 U_1^T ... x_d U_d^T.
+    """
+    b = np.asarray(a, dtype=np.float64)
+    qs, trs = [], []
+    for k, r in enumerate(ranks):
+        q_k, tr = _range_finder(unfold(b, k), r, p, q, seed, k + 1, shift, full=True)  # lines 3-11
+        qs.append(q_k)
+        trs.append(tr)
+        b = mode_product(b, q_k.T, k)                                                  # line 12
+    g = b
+    us = []
+    for k, r in enumerate(ranks):                                                      # line 14
+        v, _ = econ_svd(unfold(g, k))
+        v = v[:, :r]
+        u = qs[k] @ v                                                                  # line 15
+        u_p = sign_pin(u)
+        sgn = np.where(np.sum(u_p * u, axis=0) < 0.0, -1.0, 1.0)
+        us.append(u_p)
+        g = mode_product(g, (v * sgn).T, k)
     return Result(g, us, trs)

@@ -366,3 +366,68 @@ def test_pve_tensor_b_reaches_closed_form(kind):
             re = metrics.relative_error(a, res.core, res.factors)
             assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (kind, r, tol, re, cf)
             assert all(2 <= t.q <= 30 for t in res.traces)
+
+
+# ------------------------------------------------------------ Alg. A.2 (holistic ST-HOSVD)
+def test_a2_full_width_is_deterministic_sthosvd():
+    """l_k = n_k: every Q_k is square orthogonal, B = A x_k Q_k^T is a rotation of A, and
+    lines 14-15 reproduce Alg. 1's ST-HOSVD of A (U_k = Q_k V_k spans A's own singular
+    subspaces; both sides sign-pinned)."""
+    rng = np.random.default_rng(41)
+    dims, ranks = (8, 8, 8), (3, 3, 3)        # one shared p = 5 gives l_k = 8 = n_k
+    a = rng.standard_normal(dims) * np.exp(-0.4 * np.indices(dims).sum(axis=0))
+    det_core, det_us = tucker.thosvd(a, ranks, sequential=True)
+    res = tucker.rsthosvd_a2(a, ranks, p=5, q=2, seed=3)
+    for u_d, u_a in zip(det_us, res.factors):
+        np.testing.assert_allclose(u_a, u_d, atol=1e-10)
+    np.testing.assert_allclose(res.core, det_core, atol=1e-10)
+
+
+def test_a2_core_identity_and_orthonormality():
+    """core = A x_1 U_1^T ... x_d U_d^T (recomputed directly) and U_k^T U_k = I."""
+    rng = np.random.default_rng(42)
+    dims = (14, 12, 10, 9)
+    a = rng.standard_normal(dims) * np.exp(-0.3 * np.indices(dims).sum(axis=0))
+    res = tucker.rsthosvd_a2(a, (3, 4, 2, 3), p=3, q=2, seed=8)
+    g = a
+    for k, u in enumerate(res.factors):
+        assert metrics.orthonormality(u) <= 1e-12
+        g = tucker.mode_product(g, u.T, k)
+    np.testing.assert_allclose(res.core, g, atol=1e-12)
+
+
+@pytest.mark.parametrize("shift", [True, False])
+def test_a2_exact_recovery(shift):
+    """A rank-(3,2,4) Tucker tensor is recovered exactly when l_k > r_k (RE at rounding)."""
+    rng = np.random.default_rng(43)
+    dims, ranks = (15, 13, 11), (3, 2, 4)
+    core = rng.standard_normal(ranks)
+    us = [orthonormal_factor(n, r, rng) for n, r in zip(dims, ranks)]
+    a = tucker_tensor(core, us, dtype=np.float64)
+    res = tucker.rsthosvd_a2(a, ranks, p=2, q=1, seed=4, shift=shift)
+    assert metrics.relative_error(a, res.core, res.factors) <= 1e-10
+
+
+def test_a2_mode1_range_finder_is_algorithm_4s():
+    """Mode 1 of A.2 factors A_(1) with the same Omega_1 as Alg. 4: identical shift trace
+    and the same leading subspace (lines 3-11 = Alg. 4 lines 3-11)."""
+    rng = np.random.default_rng(44)
+    dims = (20, 16, 12)
+    a = rng.standard_normal(dims) * np.exp(-0.25 * np.indices(dims).sum(axis=0))
+    r4 = tucker.rsthosvd(a, (4, 3, 3), p=3, q=3, seed=6)
+    ra = tucker.rsthosvd_a2(a, (4, 3, 3), p=3, q=3, seed=6)
+    assert ra.traces[0].alpha == r4.traces[0].alpha
+    assert ra.traces[0].sigma_ll == r4.traces[0].sigma_ll
+
+
+@pytest.mark.parametrize("kind", ["slow", "fast"])
+def test_a2_tensor_b_reaches_closed_form(kind):
+    """On tensor B A.2 reaches the closed-form optimum (>= it, within 1e-3)."""
+    from workloads import make_tensor_b, tensor_b_spectrum
+    a = make_tensor_b(50, kind, 9).astype(np.float64)
+    v = tensor_b_spectrum(50, kind)
+    for r in (6, 12):
+        cf = np.sqrt(np.sum(v[r:] ** 2) / np.sum(v ** 2))
+        res = tucker.rsthosvd_a2(a, (r, r, r), 5, 2, 3)
+        re = metrics.relative_error(a, res.core, res.factors)
+        assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (kind, r, re, cf)
