@@ -69,7 +69,7 @@ typedef struct rtk_report {
   int32_t numeric;      /* out   : 0 ok, else RTK_ERR_NUMERIC                              */
 } rtk_report;
 
-/* Solver options for rtk_solve (defaults: {1, 1, 0.0, 0}). */
+/* Solver options for rtk_solve (defaults: {1, 1, 0.0, 0, 0}). */
 typedef struct rtk_options {
   int32_t sequential; /* 0: T-HOSVD (Alg. 3, every mode factors A_(k)); 1: ST-HOSVD (Alg. 4) */
   int32_t shift;      /* 1: adaptive shift (Alg. 3/4); 0: alpha == 0 (Alg. 2)                */
@@ -79,6 +79,12 @@ typedef struct rtk_options {
                        * sigma_{r_k+1}.  RTK_ERR_ARG unless sequential, p >= 1, r_k+p <= 64.
                        * q_used / alpha_trace report the steps taken (trace zero past them). */
   int32_t path;       /* 0: auto, 1: FP32 FFMA tiles, 2: tcgen05 3xTF32 (RTK_ERR_SHAPE if n/a)  */
+  int32_t variant;    /* 0: Alg. 2/3/4 as selected above; 1: Alg. A.2 (A.1 with
+                       * shift = 0): every mode keeps all l_k = r_k + p columns (B = B x_k Q_k^T),
+                       * then a deterministic fp64 ST-HOSVD of the l_1 x ... x l_d tensor gives
+                       * V_k and U_k = Q_k V_k (sign pin C6).  Needs sequential = 1, pve_tol = 0,
+                       * l_k <= 64 and l_k <= min(n_k, m_k) with m_k over l_1..l_{k-1}
+                       * (RTK_ERR_ARG / RTK_ERR_SHAPE otherwise). */
 } rtk_options;
 
 /*
@@ -111,7 +117,7 @@ RTK_API int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dim
               const int32_t* ranks, int32_t p, int32_t q, uint64_t seed, float* const* U,
               float* core, void* ws, size_t ws_bytes, void* stream, rtk_report* rep);
 
-/* Workspace bytes for (algo: 0 = T-HOSVD, 1 = ST-HOSVD).  Returns 0 on invalid
+/* Workspace bytes for (algo: 0 = T-HOSVD, 1 = ST-HOSVD, 2 = Alg. A.2).  Returns 0 on invalid
  * arguments (message in rtk_last_error()). */
 RTK_API size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks,
                            int32_t p, int32_t q);

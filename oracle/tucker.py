@@ -195,12 +195,17 @@ def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = T
     Line 14: deterministic ST-HOSVD of the l_1 x ... x l_d tensor B (Alg. 1, ST branch):
     V_k = first r_k left singular vectors of G_(k), G = G x_k V_k^T.
     Line 15: U_k = Q_k V_k, sign-pinned (C6); V_k's columns carry the same signs so that the
-    core stays G = A x_1 U_1^T ... x_d U_d^T.
+    core stays G = A x_1 U_1^T ... x_d U_d^T.  Q_k itself is sign-pinned column by column
+    before line 12 (reading C18: the paper's svd leaves the signs open, and they change
+    the next mode's Gaussian sketch).
     """
     b = np.asarray(a, dtype=np.float64)
     qs, trs = [], []
     for k, r in enumerate(ranks):
         q_k, tr = _range_finder(unfold(b, k), r, p, q, seed, k + 1, shift, full=True)  # lines 3-11
+        # the next mode's sketch B_(k+1) Omega_{k+1} sees Q_k's column signs (not only its
+        # span): pin all l_k columns as C6 pins U_k (DESIGN.md reading C18)
+        q_k = sign_pin(q_k)
         qs.append(q_k)
         trs.append(tr)
         b = mode_product(b, q_k.T, k)                                                  # line 12

@@ -37,7 +37,7 @@ class ProfStats(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("sequential", ctypes.c_int32), ("shift", ctypes.c_int32),
-                ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32)]
+                ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32), ("variant", ctypes.c_int32)]
 
 
 def lib_path() -> str:
@@ -130,12 +130,12 @@ def _is_column_major(x) -> bool:
     return True
 
 
-def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int) -> int:
+def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int, variant: int = 0) -> int:
     lib = load_library()
     d = len(dims)
     dd = (ctypes.c_int64 * d)(*dims)
     rr = (ctypes.c_int32 * d)(*ranks)
-    n = lib.rtk_workspace_bytes(1 if sequential else 0, dd, d, rr, p, q)
+    n = lib.rtk_workspace_bytes(2 if variant == 1 else (1 if sequential else 0), dd, d, rr, p, q)
     if n == 0:
         raise RtkError(1, lib.rtk_last_error().decode())
     return int(n)
@@ -171,11 +171,13 @@ _WS = _WorkspaceCache()
 
 
 def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: bool = True,
-          report: bool = False, out=None, workspace=None, pve_tol: float = 0.0, path: int = 0):
+          report: bool = False, out=None, workspace=None, pve_tol: float = 0.0, path: int = 0,
+          variant: int = 0):
     """General solver: Alg. 4 (sequential) / Alg. 3 (not sequential); shift=False is Alg. 2.
 
     pve_tol > 0 selects Alg. B.1 (PAPER.md:1145-1172) with q as q_max (sequential only);
     path: 0 auto, 1 FP32 FFMA tiles, 2 tcgen05 3xTF32 (rtk_options.path).
+    variant=1 selects Alg. A.2 (shift=False gives Alg. A.1).
 
     Returns (core, [U_1..U_d]) or (core, U, Report) with report=True.
     ``out=(core, [U_k])`` reuses caller-allocated outputs (column-major).
@@ -202,9 +204,9 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     dd = (ctypes.c_int64 * d)(*dims)
     rr = (ctypes.c_int32 * d)(*ranks)
     up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
-    ws_bytes = workspace_bytes(sequential, dims, ranks, p, q) if min(ranks) >= 1 else 0
+    ws_bytes = workspace_bytes(sequential, dims, ranks, p, q, variant) if min(ranks) >= 1 else 0
     ws = workspace if workspace is not None else _WS.get(dev, max(ws_bytes, 1))
-    opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path))
+    opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path), int(variant))
     rep = None
     bufs = None
     if report:
@@ -240,6 +242,12 @@ def rthosvd(A, ranks, p: int, q: int, seed: int, **kw):
 def rsthosvd(A, ranks, p: int, q: int, seed: int, **kw):
     """Shifted randomized ST-HOSVD, Alg. 4 -> rtk_rsthosvd semantics."""
     return solve(A, ranks, p, q, seed, sequential=True, **kw)
+
+
+def rsthosvd_a2(A, ranks, p: int, q: int, seed: int, **kw):
+    """Holistic shifted randomized ST-HOSVD, Alg. A.2 -> rtk_solve with
+    variant = 1 (shift=False: Alg. A.1)."""
+    return solve(A, ranks, p, q, seed, sequential=True, variant=1, **kw)
 
 
 def omega(seed: int, mode: int, row0: int, rows: int, l: int, device="cuda"):

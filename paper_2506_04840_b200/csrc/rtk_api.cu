@@ -72,14 +72,21 @@ struct Problem {
   int p = 0, q = 0;
   bool seq = true;
   double pve = 0.0;   // > 0: Alg. B.1 tolerance, q is q_max
+  bool a2 = false;    // Alg. A.2: each mode keeps all l_k columns, then ST-HOSVD of the l-core
+  std::vector<int> keep;   // columns kept by mode k's shrink: r_k, or l_k = r_k + p (A.2)
 };
+
+void set_keep(Problem& P) {
+  P.keep.resize(P.d);
+  for (int k = 0; k < P.d; ++k) P.keep[k] = P.ranks[k] + (P.a2 ? P.p : 0);
+}
 
 // m_k: columns of the matrix mode k factors (PAPER.md:257 vs :300)
 int64_t mode_cols(const Problem& P, int k) {
   int64_t m = 1;
   for (int j = 0; j < P.d; ++j) {
     if (j == k) continue;
-    m *= (P.seq && j < k) ? P.ranks[j] : P.dims[j];
+    m *= (P.seq && j < k) ? P.keep[j] : P.dims[j];
   }
   return m;
 }
@@ -99,6 +106,7 @@ int validate(const Problem& P) {
       return fail(RTK_ERR_SHAPE, "l_k = r_k + p exceeds min(n_k, m_k) in mode " + std::to_string(k + 1) +
                                      " (PAPER.md:272)");
     if (l > kLMaxApi) return fail(RTK_ERR_SHAPE, "l_k > 96 is not supported by the one-CTA small solves");
+    if (P.a2 && l > kSolveLMax) return fail(RTK_ERR_SHAPE, "Alg. A.2 needs l_k = r_k + p <= 64");
     if (P.dims[k] > kNMax) return fail(RTK_ERR_SHAPE, "n_k > 4096 is not supported by the tile kernels");
   }
   return RTK_OK;
@@ -132,7 +140,7 @@ View shrink_view(const Problem& P, int k, const float* A, const float* buf) {
   v.P = 1;
   int64_t m = 1;
   for (int j = 0; j < P.d; ++j)
-    if (j != k) m *= (j < k) ? P.ranks[j] : P.dims[j];
+    if (j != k) m *= (j < k) ? P.keep[j] : P.dims[j];
   v.S = m;
   v.sp = 1; v.si = 1;
   if (k == 0) { v.base = A; v.ss = P.dims[0]; }
@@ -147,6 +155,7 @@ struct Layout {
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
   size_t g2part = 0, gsum = 0, amax = 0;
+  size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
   size_t shr_elems = 0;
   std::vector<TilePlan> sk, pw, sh;
 };
@@ -170,7 +179,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
     svp.base = k == 0 ? A : (const float*)nullptr;
     if (path != 1) {
       L.tc_range[k] = tc_supported(rvp, l) ? 1 : 0;
-      L.tc_shrink[k] = tc_supported(svp, P.ranks[k]) ? 1 : 0;
+      L.tc_shrink[k] = tc_supported(svp, P.keep[k]) ? 1 : 0;
     }
     if (L.tc_range[k]) {
       const int N = tc_npad(l), nit = (rv.n + 127) / 128;
@@ -179,11 +188,11 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
       ldw = std::max<int64_t>(ldw, pad4(rv.m()));
       wbuf = std::max(wbuf, (size_t)2 * N * pad4(rv.m()));
     }
-    if (L.tc_shrink[k]) planes = std::max(planes, (size_t)2 * tc_npad(P.ranks[k]) * pad4(rv.n));
+    if (L.tc_shrink[k]) planes = std::max(planes, (size_t)2 * tc_npad(P.keep[k]) * pad4(rv.n));
     L.sk[k] = plan_tile(rv, l, OP_SKETCH, nsm);
     L.pw[k] = plan_tile(rv, l, OP_POWER, nsm);
     View sv = shrink_view(P, k, nullptr, nullptr);
-    L.sh[k] = plan_tile(sv, P.ranks[k], OP_SHRINK, nsm);
+    L.sh[k] = plan_tile(sv, P.keep[k], OP_SHRINK, nsm);
     for (const TilePlan* tp : {&L.sk[k], &L.pw[k]})
       ypart = std::max(ypart, (size_t)tp->G * tp->ltot() * tp->n_rows());
     const size_t n = (size_t)P.dims[k];
@@ -196,7 +205,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
     if (k + 1 < P.d) {
       // output of shrink k: (r_1..r_k) x pad4(n_{k+1}) x (n_{k+2}..n_d)
       size_t e = (size_t)pad4(P.dims[k + 1]);
-      for (int j = 0; j <= k; ++j) e *= P.ranks[j];
+      for (int j = 0; j <= k; ++j) e *= P.keep[j];
       for (int j = k + 2; j < P.d; ++j) e *= P.dims[j];
       shr = std::max(shr, e);
     }
@@ -225,6 +234,16 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.amax = take((size_t)8 * 2 * kSolveLMax * 8);
   L.shr0 = take(shr * 4);
   L.shr1 = take(shr * 4);
+  if (P.a2) {
+    size_t qa = 0, lt = 1;
+    for (int k = 0; k < P.d; ++k) { qa += (size_t)P.dims[k] * P.keep[k]; lt *= (size_t)P.keep[k]; }
+    L.a2q = take(qa * 8);
+    L.a2b = take(lt * 4);
+    L.a2g0 = take(lt * 8);
+    L.a2g1 = take(lt * 8);
+    L.a2gram = take((size_t)kSolveLMax * kSolveLMax * 8);
+    L.a2v = take((size_t)kSolveLMax * kSolveLMax * 8);
+  }
   L.total = off;
   return L;
 }
@@ -265,7 +284,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
              bool shift, float* Uk, cudaStream_t st) {
   const int n = v.n, r = P.ranks[k], l = r + P.p;
   ModeBufs B;
-  B.n = n; B.l = l; B.r = r;
+  B.n = n; B.l = l; B.r = P.a2 ? l : r;   // A.2: the step kernel pins all l columns of Q
   B.Ypart = (float*)(ws + L.ypart);
   B.Y = (double*)(ws + L.y);
   B.Q1 = (double*)(ws + L.q1);
@@ -362,8 +381,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         g_launches += 1;
       }
       // B.1 may stop at any power step: U_k is written by the step that stops (or the last)
-      RTK_CK(launch_step(B, step, P.q, shift, (step == P.q || (pve && step > 0)) ? Uk : nullptr, seed, mode1,
-                         planes, tc_npad(l), (int)pad4(n), dstep, pve ? P.pve : 0.0, st));
+      // A.2: the pinned fp32 basis replaces the shadow Qs (the shrink's matrix), Qd pinned in place
+      float* uout = P.a2 ? (float*)(ws + L.qs) : Uk;
+      RTK_CK(launch_step(B, step, P.q, shift, (step == P.q || (pve && step > 0)) ? uout : nullptr, seed, mode1,
+                         planes, tc_npad(l), (int)pad4(n), dstep, pve ? P.pve : 0.0, st, P.a2));
       g_launches += 2;
     } else {
       ProfScope ps(3, k, st);
@@ -389,30 +410,31 @@ int run_shrink(const Problem& P, const Layout& L, char* ws, int k, const View& v
   T.v = v;
   T.op = OP_SHRINK;
   T.tp = L.sh[k];
-  T.l = P.ranks[k];
+  T.l = P.keep[k];
   T.Q = Uk;
   T.qld = (int)P.dims[k];
   int64_t Rprev = 1;
-  for (int j = 0; j < k; ++j) Rprev *= P.ranks[j];
+  for (int j = 0; j < k; ++j) Rprev *= P.keep[j];
   T.Rprev = Rprev;
   if (k + 1 < P.d) { T.nnext = P.dims[k + 1]; T.ldnext = pad4(P.dims[k + 1]); }
   else { T.nnext = 1; T.ldnext = 1; }
   T.out = out;
   ProfScope ps(2, k, st);
   const char* fz = getenv("RTK_FUSED");
-  if (L.tc_shrink[k] && tc_supported(v, P.ranks[k]) && !(fz && fz[0] == '0') && fused_supported(v, P.ranks[k])) {
+  const int kk = P.keep[k];
+  if (L.tc_shrink[k] && tc_supported(v, kk) && !(fz && fz[0] == '0') && fused_supported(v, kk)) {
     float* planes = (float*)(ws + L.planes);
-    RTK_CK(tc_split(nullptr, Uk, v.n, P.ranks[k], planes, st));
+    RTK_CK(tc_split(nullptr, Uk, v.n, kk, planes, st));
     int Gf = 0, rows = 0;
-    RTK_CK(fused_power(v, P.ranks[k], planes, (int)pad4(v.n), false, 0, 0, nullptr, num_sms(), &Gf, &rows, st, out,
+    RTK_CK(fused_power(v, kk, planes, (int)pad4(v.n), false, 0, 0, nullptr, num_sms(), &Gf, &rows, st, out,
                        T.Rprev, T.nnext, T.ldnext));
     g_launches += 2;
     return RTK_OK;
   }
-  if (L.tc_shrink[k] && tc_supported(v, P.ranks[k])) {
+  if (L.tc_shrink[k] && tc_supported(v, kk)) {
     float* planes = (float*)(ws + L.planes);
-    RTK_CK(tc_split(nullptr, Uk, v.n, P.ranks[k], planes, st));
-    RTK_CK(tc_op1(v, P.ranks[k], planes, nullptr, 0, true, out, T.Rprev, T.nnext, T.ldnext, st));
+    RTK_CK(tc_split(nullptr, Uk, v.n, kk, planes, st));
+    RTK_CK(tc_op1(v, kk, planes, nullptr, 0, true, out, T.Rprev, T.nnext, T.ldnext, st));
     g_launches += 2;
     return RTK_OK;
   }
@@ -430,6 +452,11 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   P.d = d; P.p = p; P.q = q; P.seq = opt.sequential != 0;
   P.dims.assign(dims, dims + d);
   P.ranks.assign(ranks, ranks + d);
+  if (opt.variant < 0 || opt.variant > 1) return fail(RTK_ERR_ARG, "variant must be 0 (Alg. 2/3/4) or 1 (Alg. A.2)");
+  P.a2 = opt.variant == 1;
+  if (P.a2 && !P.seq) return fail(RTK_ERR_ARG, "Alg. A.2 is the sequential (ST-HOSVD) variant: set sequential = 1");
+  if (P.a2 && opt.pve_tol > 0.0) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) is stated for Alg. 4, not Alg. A.2");
+  set_keep(P);
   for (int k = 0; k < d; ++k)
     if (!U[k]) return fail(RTK_ERR_ARG, "NULL U[k]");
   int rc = validate(P);
@@ -461,7 +488,31 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   RTK_CK(cudaMemsetAsync(ws + L.trace, 0, (size_t)d * q * 8, st));
   float* shr[2] = {(float*)(ws + L.shr0), (float*)(ws + L.shr1)};
   const bool shift = opt.shift != 0;
-  if (P.seq) {
+  if (P.a2) {
+    // Alg. A.2: mode k runs Alg. 4's shifted range finder on B_(k) and
+    // keeps all l_k columns, B = B x_k Q_k^T (U[k] is scratch until a2_finish writes it)
+    std::vector<double*> qk(d);
+    size_t qoff = 0;
+    for (int k = 0; k < d; ++k) {
+      const float* cur = k == 0 ? A : shr[(k - 1) & 1];
+      const View rv = range_view(P, k, A, cur);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      if (rc) return rc;
+      qk[k] = (double*)(ws + L.a2q) + qoff;
+      qoff += (size_t)P.dims[k] * P.keep[k];
+      RTK_CK(cudaMemcpyAsync(qk[k], ws + L.qd, (size_t)P.dims[k] * P.keep[k] * 8, cudaMemcpyDeviceToDevice, st));
+      const View sv = shrink_view(P, k, A, cur);
+      rc = run_shrink(P, L, ws, k, sv, (const float*)(ws + L.qs), k + 1 < d ? shr[k & 1] : (float*)(ws + L.a2b), st);
+      if (rc) return rc;
+    }
+    {   // lines 14-15: ST-HOSVD of the l_1 x ... x l_d tensor, U_k = Q_k V_k
+      ProfScope ps(3, d - 1, st);
+      RTK_CK(a2_finish((const float*)(ws + L.a2b), d, P.keep.data(), P.ranks.data(), P.dims.data(), qk.data(),
+                       (double*)(ws + L.a2g0), (double*)(ws + L.a2g1), (double*)(ws + L.a2gram),
+                       (double*)(ws + L.a2v), U, core, st));
+      g_launches += 2 + 4 * d;
+    }
+  } else if (P.seq) {
     // Alg. 4: factor G_(k), then G = G x_k U_k^T
     for (int k = 0; k < d; ++k) {
       const float* cur = k == 0 ? A : shr[(k - 1) & 1];
@@ -518,7 +569,7 @@ extern "C" {
 int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
               int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws,
               size_t ws_bytes, void* stream, rtk_report* rep) {
-  rtk_options o = {1, 1, 0.0, 0};
+  rtk_options o = {1, 1, 0.0, 0, 0};
   if (opt) o = *opt;
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
@@ -526,14 +577,14 @@ int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32
 int rtk_rthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                 int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                 void* stream, rtk_report* rep) {
-  rtk_options o = {0, 1, 0.0, 0};
+  rtk_options o = {0, 1, 0.0, 0, 0};
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
 int rtk_rsthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                  int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                  void* stream, rtk_report* rep) {
-  rtk_options o = {1, 1, 0.0, 0};
+  rtk_options o = {1, 1, 0.0, 0, 0};
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
@@ -545,8 +596,10 @@ size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const i
   }
   Problem P;
   P.d = d; P.p = p; P.q = q; P.seq = algo != 0;
+  P.a2 = algo == 2;
   P.dims.assign(dims, dims + d);
   P.ranks.assign(ranks, ranks + d);
+  set_keep(P);
   if (validate(P)) return 0;
   return plan(P, num_sms(), nullptr, 0).total;
 }

@@ -99,8 +99,13 @@ extern double* g_step_dbg;
 size_t solve_gpart_doubles(int n, int l);      // Gram partials of reduce_gram_kernel
 cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop = nullptr);
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
-                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st);
+                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st,
+                        bool pin_q = false);
 cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t st);
+// Alg. A.2 lines 14-15 (rtk_solve.cu): deterministic ST-HOSVD of the l_1 x ... x l_d fp32 tensor B
+// and U_k = Q_k V_k (sign-pinned); g0/g1 hold prod(l) doubles each, gram/V 64*64 doubles.
+cudaError_t a2_finish(const float* B, int d, const int* l, const int* r, const int64_t* n, double* const* Qk,
+                      double* g0, double* g1, double* gram, double* V, float* const* U, float* core, cudaStream_t st);
 
 // ---- tcgen05 3xTF32 path (rtk_tc.cu) -------------------------------------------
 int tc_npad(int l);                                   // l padded to the UMMA N (16..64), 0 if > 64

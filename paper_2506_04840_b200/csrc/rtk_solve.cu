@@ -641,6 +641,7 @@ struct StepArgs {
   int defer_alpha;          // non-final steps: the shift update runs in alpha_kernel (side stream)
   double pve_tol;           // > 0: Alg. B.1 stopping rule on power steps
   double* sighat;           // [kSL] B.1 sigma-hat of the previous power step (zero at mode start)
+  int pin_q;                // Alg. A.2: U = sign-pinned Q (all l columns) and Qd pinned in place
 };
 
 struct StepSmem {
@@ -1082,7 +1083,14 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
         if (v > best || (v == best && iv < bi)) { best = v; bi = iv; }
       }
       const double sgn = ldcg(a.Qd + (int64_t)c * n + bi) < 0.0 ? -1.0 : 1.0;
+      if (lane == 0) S.colscale[c] = sgn;
       for (int i = r0 + lane; i < r1; i += 32) a.U[(int64_t)c * n + i] = (float)(sgn * a.Qd[(int64_t)c * n + i]);
+    }
+    if (a.pin_q) {   // Alg. A.2: the fp64 basis takes the same signs (after every CTA read its pivot)
+      __syncthreads();
+      cluster.sync();
+      for (int c = warp; c < a.r; c += kST / 32)
+        for (int i = r0 + lane; i < r1; i += 32) a.Qd[(int64_t)c * n + i] *= S.colscale[c];
     }
   }
 }
@@ -1153,6 +1161,194 @@ cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t s
   return cudaGetLastError();
 }
 
+// ============================================================== Alg. A.2 lines 14-15
+// Deterministic ST-HOSVD (Alg. 1, ST branch) of the small l_1 x ... x l_d tensor B that the
+// holistic mode loop leaves, and U_k = Q_k V_k.  fp64 throughout;
+// every reduction has a fixed order.  The tensor is column-major; around mode k its extents are
+// (P, c, S): element (a, i, b) at a + P (i + c b).
+
+// gram(i, j) = sum_{a,b} T(a, i, b) T(a, j, b): one CTA per packed upper entry (i <= j)
+__global__ void __launch_bounds__(kST) a2_gram_kernel(const double* __restrict__ T, int64_t P, int c, int64_t S,
+                                                      double* __restrict__ gram) {
+  __shared__ double red[kST / 32];
+  int i, j;
+  unpack_upper((int)blockIdx.x, i, j);
+  double s = 0.0;
+  const int64_t tot = P * S;
+  for (int64_t t = threadIdx.x; t < tot; t += kST) {
+    const int64_t a = t % P, b = t / P;
+    s = fma(T[a + P * (i + (int64_t)c * b)], T[a + P * (j + (int64_t)c * b)], s);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kST / 32; ++w) t += red[w];
+    gram[i * c + j] = t;
+    gram[j * c + i] = t;
+  }
+}
+
+struct A2Smem {
+  double G[kSL * kLD], R[kSL * kLD], H[kSL * kLD];
+  double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL], pbuf[kSL], xrow[kSL];
+  double scal[32], dbuf[4], dots[kSL];
+  int cnt[kST];
+  int ibuf[4];
+};
+
+// V = the r leading eigenvectors of the c x c Gram (descending eigenvalues) = the leading left
+// singular vectors of T_(k): tridiagonalisation, Sturm bisection, inverse iteration and back-
+// transformation (the step kernel's eigen path), then two classical Gram-Schmidt passes in
+// descending order so that clustered eigenvalues still give an orthonormal V.
+__global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict__ gram, int c, int r,
+                                                       double* __restrict__ V) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  A2Smem& S = *reinterpret_cast<A2Smem*>(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < c * c; idx += kST) S.G[(idx / c) * kLD + idx % c] = gram[idx];
+  __syncthreads();
+  tridiag(S.G, c, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+  for (int k = tid; k + 1 < c; k += kST) S.e2[k] = S.e[k] * S.e[k];
+  __syncthreads();
+  all_eigs(S.d, S.e, S.e2, c, S.lam, S.blo, S.bhi, S.cnt);
+  double* Z = S.G;
+  tri_eigvecs(S.d, S.e, S.lam, c, Z, S.R);
+  back_transform(S.H, S.hb, c, Z);
+  // descending order into R: R(i, cc) = Z(i, c-1-cc)
+  for (int idx = tid; idx < c * r; idx += kST) {
+    const int i = idx % c, cc = idx / c;
+    S.R[i * kLD + cc] = Z[i * kLD + (c - 1 - cc)];
+  }
+  __syncthreads();
+  for (int cc = 0; cc < r; ++cc) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int jj = warp; jj < cc; jj += kST / 32) {   // dots with the finished columns
+        double t = 0.0;
+        for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + jj], S.R[i * kLD + cc], t);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) S.dots[jj] = t;
+      }
+      __syncthreads();
+      if (tid < c) {
+        double x = S.R[tid * kLD + cc];
+        for (int jj = 0; jj < cc; ++jj) x = fma(-S.dots[jj], S.R[tid * kLD + jj], x);
+        S.R[tid * kLD + cc] = x;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      double t = 0.0;
+      for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + cc], S.R[i * kLD + cc], t);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) S.dbuf[0] = t > 0.0 ? 1.0 / sqrt(t) : 0.0;
+    }
+    __syncthreads();
+    if (tid < c) S.R[tid * kLD + cc] *= S.dbuf[0];
+    __syncthreads();
+  }
+  for (int idx = tid; idx < c * r; idx += kST) V[idx] = S.R[(idx % c) * kLD + idx / c];
+}
+
+// U(:, cc) = s Q_k V(:, cc) with the sign pin s (largest |entry| positive, lowest row on ties,
+// SPEC.md:232); V(:, cc) *= s so that the core keeps G = A x_k U_k^T.  One CTA per column.
+__global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q, int n, int l,
+                                                   double* __restrict__ V, int r, float* __restrict__ U) {
+  __shared__ double vs[kSL];
+  __shared__ double bv[kST / 32];
+  __shared__ int bi[kST / 32];
+  const int cc = blockIdx.x, tid = threadIdx.x;
+  if (tid < l) vs[tid] = V[tid + (int64_t)l * cc];
+  __syncthreads();
+  double best = -1.0, bval = 0.0;
+  int bidx = 0x7fffffff;
+  for (int i = tid; i < n; i += kST) {
+    double u = 0.0;
+    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+    if (fabs(u) > best) { best = fabs(u); bidx = i; bval = u; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    const double ov = __shfl_xor_sync(0xffffffffu, bval, o);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; bval = ov; }
+  }
+  if ((tid & 31) == 0) { bv[tid >> 5] = (bval < 0.0) ? -best : best; bi[tid >> 5] = bidx; }
+  __syncthreads();
+  __shared__ double sgn_s;
+  if (tid == 0) {
+    double b = -1.0, v = 0.0;
+    int ix = 0x7fffffff;
+    for (int w = 0; w < kST / 32; ++w)
+      if (fabs(bv[w]) > b || (fabs(bv[w]) == b && bi[w] < ix)) { b = fabs(bv[w]); ix = bi[w]; v = bv[w]; }
+    sgn_s = v < 0.0 ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  const double sgn = sgn_s;
+  for (int i = tid; i < n; i += kST) {
+    double u = 0.0;
+    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+    U[i + (int64_t)n * cc] = (float)(sgn * u);
+  }
+  if (tid < l) V[tid + (int64_t)l * cc] = sgn * vs[tid];
+}
+
+// out(a, i', b) = sum_i V(i, i') T(a, i, b): extents (P, c, S) -> (P, r, S)
+__global__ void __launch_bounds__(kST) a2_modeprod_kernel(const double* __restrict__ T, int64_t P, int c, int64_t S,
+                                                          const double* __restrict__ V, int r, double* __restrict__ out) {
+  const int64_t tot = P * r * S;
+  for (int64_t idx = (int64_t)blockIdx.x * kST + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * kST) {
+    const int64_t a = idx % P, tmp = idx / P;
+    const int ip = (int)(tmp % r);
+    const int64_t b = tmp / r;
+    double s = 0.0;
+    for (int i = 0; i < c; ++i) s = fma(V[i + (int64_t)c * ip], T[a + P * (i + (int64_t)c * b)], s);
+    out[idx] = s;
+  }
+}
+
+__global__ void a2_widen_kernel(const float* __restrict__ x, int64_t n, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (double)x[i];
+}
+__global__ void a2_narrow_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
+}
+
+cudaError_t a2_finish(const float* B, int d, const int* l, const int* r, const int64_t* n, double* const* Qk,
+                      double* g0, double* g1, double* gram, double* V, float* const* U, float* core, cudaStream_t st) {
+  int64_t ext[8], tot = 1;
+  for (int k = 0; k < d; ++k) { ext[k] = l[k]; tot *= l[k]; }
+  const int gs = (int)std::min<int64_t>(4096, (tot + 255) / 256);
+  a2_widen_kernel<<<gs, 256, 0, st>>>(B, tot, g0);
+  const size_t smem = sizeof(A2Smem);
+  cudaError_t e = cudaFuncSetAttribute(a2_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  for (int k = 0; k < d; ++k) {
+    int64_t P = 1, S = 1;
+    for (int j = 0; j < k; ++j) P *= ext[j];
+    for (int j = k + 1; j < d; ++j) S *= ext[j];
+    const int c = (int)ext[k];
+    a2_gram_kernel<<<c * (c + 1) / 2, kST, 0, st>>>(g0, P, c, S, gram);
+    a2_eig_kernel<<<1, kST, smem, st>>>(gram, c, r[k], V);
+    a2_u_kernel<<<r[k], kST, 0, st>>>(Qk[k], (int)n[k], c, V, r[k], U[k]);
+    const int64_t ot = P * r[k] * S;
+    a2_modeprod_kernel<<<(int)std::min<int64_t>(4096, (ot + kST - 1) / kST), kST, 0, st>>>(g0, P, c, S, V, r[k], g1);
+    std::swap(g0, g1);
+    ext[k] = r[k];
+  }
+  int64_t rt = 1;
+  for (int k = 0; k < d; ++k) rt *= r[k];
+  a2_narrow_kernel<<<(int)std::min<int64_t>(4096, (rt + 255) / 256), 256, 0, st>>>(g0, rt, core);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- host side
 double* g_step_dbg = nullptr;   // diagnostics: set by rtk_debug_clocks (not part of the product path)
 
@@ -1171,7 +1367,8 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
 }
 
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
-                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st) {
+                        float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st,
+                        bool pin_q) {
   StepArgs a;
   a.n = B.n; a.l = B.l; a.r = B.r; a.step = step; a.q = q;
   a.shift = shift ? 1 : 0; a.final_step = (step == q) ? 1 : 0;
@@ -1184,6 +1381,7 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   a.defer_alpha = defer_alpha ? 1 : 0;
   a.pve_tol = pve_tol;
   a.sighat = B.sighat;
+  a.pin_q = pin_q ? 1 : 0;
   const int C = solve_cluster_size(B.n);
   const size_t smem = sizeof(StepSmem);
   cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

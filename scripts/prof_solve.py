@@ -1,6 +1,6 @@
 """One profiled solve of a config through the public API; prints device ms by (kind, mode).
 
-python scripts/prof_solve.py [c5] [reps]
+python scripts/prof_solve.py [c5] [reps] [a2]   (a2: Alg. A.2 instead of the config's algorithm)
 """
 import json
 import os
@@ -21,6 +21,8 @@ def main():
     c = CONFIGS[name]
     A = make_config_tensor_torch(name)
     fn = rt.rsthosvd if c["algo"] == "rsthosvd" else rt.rthosvd
+    if len(sys.argv) > 3 and sys.argv[3] == "a2":
+        fn, name = rt.rsthosvd_a2, name + "-a2"
     fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"])
     torch.cuda.synchronize()
     rt.profile_begin()

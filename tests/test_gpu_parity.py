@@ -214,3 +214,80 @@ def test_pve_table_b1_tensor_b_600(kind):
         assert abs(re / cf - 1) <= 2e-3, (kind, r, tol, re, cf, rep.q_used)
         assert abs(re - re_paper) <= 0.006 * re_paper, (kind, r, tol, re, re_paper)
         print(f"tensor B {kind} r={r} tol={tol}: q_used={rep.q_used} (paper {q_paper}) RE={re:.4e} (paper {re_paper})")
+
+
+# ------------------------------------------------------------ Alg. A.2 (holistic ST-HOSVD)
+def _a2_check(a, ranks, p, q, seed, shift=True, alpha_rtol=1e-3):
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import rsthosvd_a2
+    A = to_device_colmajor(a, torch)
+    core, U, rep = rsthosvd_a2(A, ranks, p, q, seed, shift=shift, report=True)
+    torch.cuda.synchronize()
+    g_core, g_U = core.cpu().numpy(), [u.cpu().numpy() for u in U]
+    orc = tucker.rsthosvd_a2(a, ranks, p, q, seed, shift=shift)
+    assert rep.numeric == 0
+    re_g = metrics.relative_error(a, g_core, g_U)
+    re_o = metrics.relative_error(a, orc.core, orc.factors)
+    assert abs(re_g - re_o) <= RE_TOL * re_o + 1e-7, (re_g, re_o)
+    for u in g_U:
+        assert metrics.orthonormality(u) <= ORTH_TOL
+    gaps = metrics.mode_gaps(a, ranks, orc.factors, True)
+    for k, u in enumerate(g_U):
+        if gaps[k] > 0.10:
+            assert metrics.max_principal_angle(orc.factors[k], u) <= ANGLE_TOL, (k, gaps[k])
+    for k, tr in enumerate(orc.traces):
+        if tr.alpha and max(tr.alpha) > 0:
+            np.testing.assert_allclose(rep.alpha_trace[k], tr.alpha, rtol=alpha_rtol, atol=1e-12)
+    return re_g, re_o
+
+
+@pytest.mark.parametrize("path", ["ffma", "fused"])
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_a2_config_parity(cfg, path, monkeypatch):
+    """Alg. A.2 on the ST configs (reduced C3 size keeps the oracle in seconds)."""
+    monkeypatch.setenv("RTK_PATH", "ffma" if path == "ffma" else "tc")
+    monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
+    c = CONFIGS[cfg]
+    dims = (160, 150, 140) if cfg == "c3" else None
+    a = make_config_tensor(cfg, dims=dims)
+    _a2_check(a, c["ranks"], c["p"], c["q"], c["omega_seed"])
+
+
+@pytest.mark.parametrize("shift", [True, False])
+@pytest.mark.parametrize("dims,ranks,p,q", [
+    ((640, 40, 36), (20, 8, 6), 6, 3),        # n_1 > 512: 2-CTA fused cluster
+    ((37, 29, 23), (4, 5, 3), 3, 2),          # odd sizes, ragged tiles
+    ((16, 12, 10, 9), (3, 2, 4, 2), 2, 3),    # d = 4
+    ((40, 30), (6, 4), 2, 2),                 # d = 2
+])
+def test_a2_random_shapes(shift, dims, ranks, p, q):
+    rng = np.random.default_rng(sum(dims) + 7)
+    cr = tuple(min(n, r + 4) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
+    us = [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)]
+    a = tucker_tensor(core, us, noise=1e-3, rng=rng)
+    _a2_check(a, ranks, p, q, 31, shift=shift, alpha_rtol=5e-3)
+
+
+def test_a2_exact_recovery_gpu():
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import rsthosvd_a2
+    rng = np.random.default_rng(5)
+    dims, ranks = (30, 26, 22), (3, 4, 2)
+    a = tucker_tensor(rng.standard_normal(ranks), [orthonormal_factor(n, r, rng) for n, r in zip(dims, ranks)])
+    A = to_device_colmajor(a, torch)
+    core, U = rsthosvd_a2(A, ranks, 3, 2, 5)
+    re = metrics.relative_error(a, core.cpu().numpy(), [u.cpu().numpy() for u in U])
+    assert re < 1e-5
+    for u in U:
+        assert metrics.orthonormality(u.cpu().numpy()) <= ORTH_TOL
+
+
+def test_a2_rejected_where_undefined():
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import solve
+    A = to_device_colmajor(np.random.default_rng(0).standard_normal((20, 18, 16)), torch)
+    with pytest.raises(Exception):
+        solve(A, (3, 3, 3), 2, 2, 1, sequential=False, variant=1)     # A.2 is ST only
+    with pytest.raises(Exception):
+        solve(A, (3, 3, 3), 2, 2, 1, sequential=True, variant=1, pve_tol=0.1)
