@@ -180,3 +180,84 @@ def omega(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
     out[:, 2::4] = z2
     out[:, 3::4] = z3
     return out[:, :l].astype(np.float32)
+
+
+# ------------------------------------------------------------------ other sketch types
+# PAPER.md:1377-1379 (Appendix D) compares Omega_k drawn as: a standard Gaussian matrix (the
+# main algorithms, RTK-GAUSS-1 above), a uniform random matrix (entries i.i.d. U[-1, 1]), and
+# the Khatri-Rao product of standard Gaussian / uniform matrices.  The paper fixes neither a
+# generator nor the Khatri-Rao ordering; this build freezes (readings C2, C19):
+#
+# RTK-UNIF-1  counter (c // 4, lo32(j), hi32(j), 0x55000000 | k); word t of the Philox output
+#             gives column 4 (c // 4) + t:  w = 2 u - 1 = (2 (x >> 8) + 1 - 2^24) 2^-24 (exact)
+# RTK-KR-1    Omega_k(j, c) = fl32( prod_{m != k, m ascending} f_m(i_m, c) ), the product taken
+#             in binary64, where j = sum_m i_m stride_m over the unfolding's column modes
+#             (Kolda-Bader: lower modes fastest, extents of the CURRENT tensor), i.e. the
+#             Khatri-Rao product F_d (.) ... (.) F_1 without F_k.  f_m is an n_m x l matrix
+#             drawn row by row like Omega itself with counter word 3 =
+#             0x4B000000 | (m << 8) | k  (Gaussian, RTK-GAUSS-1 pairs) or
+#             0x4C000000 | (m << 8) | k  (uniform, RTK-UNIF-1 words).
+OMEGA_GAUSS, OMEGA_UNIF, OMEGA_KR_GAUSS, OMEGA_KR_UNIF = 0, 1, 2, 3
+
+
+def _philox_rows(seed: int, word3: int, row0: int, rows: int, l: int):
+    j = np.arange(row0, row0 + rows, dtype=np.uint64)[:, None]
+    c4 = np.arange((l + 3) // 4, dtype=np.uint64)[None, :]
+    k0 = np.uint64(seed & 0xFFFFFFFF)
+    k1 = np.uint64((seed >> 32) & 0xFFFFFFFF)
+    return philox4x32_10(c4, j & _MASK, j >> _S32, np.uint64(word3), k0, k1)
+
+
+def _interleave(zs, rows: int, l: int) -> np.ndarray:
+    out = np.empty((rows, 4 * zs[0].shape[1]), dtype=np.float64)
+    for t in range(4):
+        out[:, t::4] = zs[t]
+    return out[:, :l]
+
+
+def unif_sym(x):
+    """RTK-UNIF-1 value 2u - 1 for u = ((x>>8)+0.5) 2^-24 (exact in binary64 and binary32)."""
+    return (2.0 * (np.asarray(x, dtype=np.uint64) >> np.uint64(8)).astype(np.float64) + 1.0 - 2.0 ** 24) * 2.0 ** -24
+
+
+def draw_rows(seed: int, word3: int, row0: int, rows: int, l: int, uniform: bool) -> np.ndarray:
+    """Rows [row0, row0+rows) x l of one Philox stream (binary64 values before rounding)."""
+    x = _philox_rows(seed, word3, row0, rows, l)
+    if uniform:
+        return _interleave([unif_sym(v) for v in x], rows, l)
+    z0, z1 = box_muller(x[0], x[1])
+    z2, z3 = box_muller(x[2], x[3])
+    return _interleave([z0, z1, z2, z3], rows, l)
+
+
+def omega_uniform(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
+    """Rows of a uniform U[-1, 1] Omega_k (RTK-UNIF-1), float32."""
+    return draw_rows(seed, 0x55000000 | mode, row0, rows, l, True).astype(np.float32)
+
+
+def kr_factor(seed: int, mode: int, fmode: int, n: int, l: int, uniform: bool) -> np.ndarray:
+    """Factor F_m (n x l, float32) of mode k's Khatri-Rao sketch (RTK-KR-1); fmode = m (1-based)."""
+    w3 = (0x4C000000 if uniform else 0x4B000000) | (fmode << 8) | mode
+    return draw_rows(seed, w3, 0, n, l, uniform).astype(np.float32)
+
+
+def sketch(kind: int, seed: int, mode: int, dims, l: int, row0: int = 0, rows=None) -> np.ndarray:
+    """Rows [row0, row0+rows) of Omega_k (float32, rows x l) for the mode-k unfolding of a tensor
+    of extents ``dims`` (d entries; mode = k, 1-based).  kind: OMEGA_* above."""
+    cm = [m for m in range(1, len(dims) + 1) if m != mode]
+    m_tot = int(np.prod([dims[m - 1] for m in cm]))
+    rows = m_tot - row0 if rows is None else rows
+    if kind == OMEGA_GAUSS:
+        return omega(seed, mode, row0, rows, l)
+    if kind == OMEGA_UNIF:
+        return omega_uniform(seed, mode, row0, rows, l)
+    uniform = kind == OMEGA_KR_UNIF
+    j = np.arange(row0, row0 + rows, dtype=np.int64)
+    prod = np.ones((rows, l), dtype=np.float64)
+    stride = 1
+    for m in cm:                                   # ascending: the fastest column mode first
+        n_m = dims[m - 1]
+        f = kr_factor(seed, mode, m, n_m, l, uniform).astype(np.float64)
+        prod = prod * f[(j // stride) % n_m, :]
+        stride *= n_m
+    return prod.astype(np.float32)

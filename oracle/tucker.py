@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .gauss import omega
+from .gauss import OMEGA_GAUSS, omega, sketch
 
 
 # ----------------------------------------------------------------- tensor ops
@@ -103,7 +103,8 @@ class Result:
 
 
 def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
-                  shift: bool, pve_tol=None, full: bool = False):
+                  shift: bool, pve_tol=None, full: bool = False, omega_kind: int = OMEGA_GAUSS,
+                  dims=None):
     """Lines 3-13 of Alg. 3 / Alg. 4 for one mode.
 
     m      : the matrix being factored, A_(k) (Alg. 3) or G_(k) (Alg. 4), float64
@@ -111,13 +112,18 @@ def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
     shift  : False -> Alg. 2 (alpha fixed at 0)
     pve_tol: (tol, q_max) -> Alg. B.1 stopping rule
     full   : return the whole n x l basis Q_k of the last iterate (Alg. A.2 line 12), unpinned
+    omega_kind, dims: sketch type (gauss.OMEGA_*) and the extents of the
+             tensor whose mode-mode1 unfolding m is (needed by the Khatri-Rao types)
     Returns (U_k sign-pinned n x r, ModeTrace), or (Q_k n x l, ModeTrace) with full=True.
     """
     n, cols = m.shape
     l = r + p
     if pve_tol is not None and p < 1:
         raise ValueError("Alg. B.1 compares against sigma_{r+1}: needs p >= 1")
-    om = omega(seed, mode1, 0, cols, l).astype(np.float64)    # line 3: Omega_k
+    if omega_kind == OMEGA_GAUSS:
+        om = omega(seed, mode1, 0, cols, l).astype(np.float64)  # line 3: Omega_k
+    else:                                                       # Appendix D types
+        om = sketch(omega_kind, seed, mode1, dims, l).astype(np.float64)
     q_mat, _ = econ_svd(m @ om)                                 # line 5
     alpha = 0.0                                                 # line 5: alpha = 0
     tr = ModeTrace(l=l)
@@ -148,7 +154,8 @@ def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
     return u, tr
 
 
-def rthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True) -> Result:
+def rthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True,
+            omega_kind: int = OMEGA_GAUSS) -> Result:
     """Alg. 3, shifted randomized T-HOSVD; shift=False is Alg. 2.
 
     Every mode factors the ORIGINAL A_(k); the core is A x_1 U_1^T ... x_d U_d^T
@@ -157,7 +164,8 @@ def rthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True)
     a64 = np.asarray(a, dtype=np.float64)
     us, trs = [], []
     for k, r in enumerate(ranks):
-        u, tr = _range_finder(unfold(a64, k), r, p, q, seed, k + 1, shift)
+        u, tr = _range_finder(unfold(a64, k), r, p, q, seed, k + 1, shift,
+                              omega_kind=omega_kind, dims=a64.shape)
         us.append(u)
         trs.append(tr)
     g = a64
@@ -167,7 +175,7 @@ def rthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True)
 
 
 def rsthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True,
-             pve=None) -> Result:
+             pve=None, omega_kind: int = OMEGA_GAUSS) -> Result:
     """Alg. 4, shifted randomized ST-HOSVD, order (1..d).
 
     shift=False is Alg. 2's ST branch; pve=(tol, q_max) is Alg. B.1 (pinned by
@@ -178,14 +186,16 @@ def rsthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True
     g = np.asarray(a, dtype=np.float64)
     us, trs = [], []
     for k, r in enumerate(ranks):
-        u, tr = _range_finder(unfold(g, k), r, p, q, seed, k + 1, shift, pve)
+        u, tr = _range_finder(unfold(g, k), r, p, q, seed, k + 1, shift, pve,
+                              omega_kind=omega_kind, dims=g.shape)
         us.append(u)
         trs.append(tr)
         g = mode_product(g, u.T, k)
     return Result(g, us, trs)
 
 
-def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True) -> Result:
+def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True,
+                omega_kind: int = OMEGA_GAUSS) -> Result:
     """Alg. A.2, holistic shifted randomized ST-HOSVD; shift=False is
     Alg. A.1.  Order 1..d.
 
@@ -202,7 +212,8 @@ def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = T
     b = np.asarray(a, dtype=np.float64)
     qs, trs = [], []
     for k, r in enumerate(ranks):
-        q_k, tr = _range_finder(unfold(b, k), r, p, q, seed, k + 1, shift, full=True)  # lines 3-11
+        q_k, tr = _range_finder(unfold(b, k), r, p, q, seed, k + 1, shift, full=True,  # lines 3-11
+                                omega_kind=omega_kind, dims=b.shape)
         # the next mode's sketch B_(k+1) Omega_{k+1} sees Q_k's column signs (not only its
         # span): pin all l_k columns as C6 pins U_k (reading C18)
         q_k = sign_pin(q_k)

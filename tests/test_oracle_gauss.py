@@ -136,3 +136,57 @@ def test_omega_golden_prefix():
         seed, mode, j, c, hexbits = int(r[0]), int(r[1]), int(r[2]), int(r[3]), r[4]
         v = g.omega(seed, mode, j, 1, c + 1)[0, c]
         assert v.view(np.uint32) == np.uint32(int(hexbits, 16)), r
+
+
+# ------------------------------------------------ Appendix D sketch types
+def test_uniform_counter_layout_via_curand(curand_host):
+    """RTK-UNIF-1 words come from the cuRAND Philox on counter (c//4, lo32 j, hi32 j,
+    0x55000000|k) and map to (2 (x>>8) + 1 - 2^24) 2^-24 (independent Philox implementation)."""
+    seed, mode, rows, l = 0x1234567890ABCDEF, 3, 7, 9
+    j0 = 2**32 - 3                                   # rows straddle the hi word of the counter
+    lines = []
+    for j in range(j0, j0 + rows):
+        for c4 in range((l + 3) // 4):
+            lines.append(f"{c4} {j & 0xffffffff} {j >> 32} {0x55000000 | mode} {seed & 0xffffffff} {seed >> 32}")
+    out = subprocess.run([curand_host], input="\n".join(lines) + "\n", capture_output=True, text=True,
+                         check=True).stdout.split()
+    words = np.array([int(t) for t in out], dtype=np.int64).reshape(rows, -1)[:, :l]
+    expect = ((2 * (words >> 8) + 1 - 2**24) / 2.0**24).astype(np.float32)
+    np.testing.assert_array_equal(g.omega_uniform(seed, mode, j0, rows, l), expect)
+
+
+def test_uniform_moments_and_ks():
+    w = g.omega_uniform(99, 2, 0, 50000, 12).astype(np.float64).ravel()
+    assert w.min() > -1.0 and w.max() < 1.0
+    assert abs(w.mean()) < 0.01 and abs(w.var() - 1.0 / 3.0) < 0.01
+    assert stats.kstest(w, "uniform", args=(-1.0, 2.0)).pvalue > 1e-3
+    assert np.all(np.mod(w * 2.0**24, 2.0) == 1.0)          # odd multiples of 2^-24
+
+
+@pytest.mark.parametrize("kind", [g.OMEGA_KR_GAUSS, g.OMEGA_KR_UNIF])
+def test_khatri_rao_structure(kind):
+    """Every column of a KR sketch, folded to the column modes' extents, is a rank-1 tensor
+    whose factors are the F_m columns (Khatri-Rao product, lower modes fastest)."""
+    dims, mode, l = (6, 5, 4, 3), 2, 7
+    om = g.sketch(kind, 5, mode, dims, l).astype(np.float64)
+    ext = [dims[m - 1] for m in (1, 3, 4)]
+    assert om.shape == (int(np.prod(ext)), l)
+    uni = kind == g.OMEGA_KR_UNIF
+    fs = [g.kr_factor(5, mode, m, dims[m - 1], l, uni).astype(np.float64) for m in (1, 3, 4)]
+    for c in range(l):
+        t = om[:, c].reshape(ext, order="F")
+        outer = np.einsum("a,b,c->abc", fs[0][:, c], fs[1][:, c], fs[2][:, c])
+        np.testing.assert_allclose(t, outer, rtol=1e-7, atol=0)
+        sv = np.linalg.svd(t.reshape(ext[0], -1, order="F"), compute_uv=False)
+        assert sv[1] <= 1e-6 * sv[0]
+
+
+def test_khatri_rao_factor_distributions():
+    fg = np.concatenate([g.kr_factor(11, 1, m, 4000, 8, False).ravel() for m in (2, 3)]).astype(np.float64)
+    assert abs(fg.mean()) < 0.02 and abs(fg.var() - 1.0) < 0.02
+    assert stats.kstest(fg, "norm").pvalue > 1e-3
+    fu = g.kr_factor(11, 1, 2, 20000, 8, True).astype(np.float64).ravel()
+    assert stats.kstest(fu, "uniform", args=(-1.0, 2.0)).pvalue > 1e-3
+    # factor streams differ by mode pair and from the dense Omega stream
+    assert not np.array_equal(g.kr_factor(11, 1, 2, 50, 8, False), g.kr_factor(11, 1, 3, 50, 8, False))
+    assert not np.array_equal(g.kr_factor(11, 1, 2, 50, 8, False), g.omega(11, 1, 0, 50, 8))

@@ -431,3 +431,32 @@ def test_a2_tensor_b_reaches_closed_form(kind):
         res = tucker.rsthosvd_a2(a, (r, r, r), 5, 2, 3)
         re = metrics.relative_error(a, res.core, res.factors)
         assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (kind, r, re, cf)
+
+
+# ------------------------------------------------------------ Appendix D sketch types
+@pytest.mark.parametrize("kind", [1, 2, 3])
+@pytest.mark.parametrize("algo", ["t", "st", "a2"])
+def test_sketch_types_exact_recovery(kind, algo):
+    """Any full-rank sketch (uniform, KR-Gaussian, KR-uniform) recovers a
+    rank-r Tucker tensor exactly when l_k > r_k."""
+    rng = np.random.default_rng(50 + kind)
+    dims, ranks = (14, 12, 10), (3, 2, 4)
+    a = tucker_tensor(rng.standard_normal(ranks), [orthonormal_factor(n, r, rng) for n, r in zip(dims, ranks)],
+                      dtype=np.float64)
+    fn = {"t": tucker.rthosvd, "st": tucker.rsthosvd, "a2": tucker.rsthosvd_a2}[algo]
+    res = fn(a, ranks, 3, 1, 12, omega_kind=kind)
+    assert metrics.relative_error(a, res.core, res.factors) <= 1e-10
+
+
+@pytest.mark.parametrize("kind", [2, 3])
+def test_kr_sketch_tensor_b_closed_form(kind):
+    """KR sketches reach tensor B's closed-form optimum like the Gaussian one (the paper's
+    Appendix D finding that the RE is comparable)."""
+    from workloads import make_tensor_b, tensor_b_spectrum
+    a = make_tensor_b(40, "slow", 13).astype(np.float64)
+    v = tensor_b_spectrum(40, "slow")
+    r = 6
+    cf = np.sqrt(np.sum(v[r:] ** 2) / np.sum(v ** 2))
+    res = tucker.rsthosvd(a, (r, r, r), 5, 2, 3, omega_kind=kind)
+    re = metrics.relative_error(a, res.core, res.factors)
+    assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (re, cf)
