@@ -85,6 +85,11 @@ typedef struct rtk_options {
                        * V_k and U_k = Q_k V_k (sign pin C6).  Needs sequential = 1, pve_tol = 0,
                        * l_k <= 64 and l_k <= min(n_k, m_k) with m_k over l_1..l_{k-1}
                        * (RTK_ERR_ARG / RTK_ERR_SHAPE otherwise). */
+  int32_t omega;      /* sketch type (Appendix D): 0 standard Gaussian
+                       * (RTK-GAUSS-1, generated inside the sketch kernels), 1 uniform U[-1,1]
+                       * (RTK-UNIF-1), 2 Khatri-Rao product of Gaussian factors, 3 Khatri-Rao
+                       * product of uniform factors (RTK-KR-1); types 1-3 are materialised once per
+                       * mode in the workspace (rtk_workspace_bytes_ex sizes it) */
 } rtk_options;
 
 /*
@@ -117,15 +122,28 @@ RTK_API int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dim
               const int32_t* ranks, int32_t p, int32_t q, uint64_t seed, float* const* U,
               float* core, void* ws, size_t ws_bytes, void* stream, rtk_report* rep);
 
-/* Workspace bytes for (algo: 0 = T-HOSVD, 1 = ST-HOSVD, 2 = Alg. A.2).  Returns 0 on invalid
- * arguments (message in rtk_last_error()). */
+/* Workspace bytes for (algo: 0 = T-HOSVD, 1 = ST-HOSVD, 2 = Alg. A.2) with the Gaussian sketch.
+ * Returns 0 on invalid arguments (message in rtk_last_error()). */
 RTK_API size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks,
                            int32_t p, int32_t q);
+
+/* Workspace bytes for rtk_solve with these options (NULL -> ST-HOSVD defaults); 0 on error. */
+RTK_API size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32_t d,
+                                      const int32_t* ranks, int32_t p, int32_t q);
 
 /* Test hook: rows [row0, row0+rows) of Omega_mode (l columns) in RTK-GAUSS-1,
  * written row-major to the DEVICE buffer out[(j-row0)*l + c] (float32). */
 RTK_API int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out,
               void* stream);
+
+/* Test hook: rows [row0, row0+rows) x l of mode `mode`'s sketch Omega_mode of type `kind` (as
+ * rtk_options.omega) for the mode-`mode` unfolding of a tensor with extents dims[0..d-1] (host;
+ * for ST modes the CURRENT extents r_1..r_{k-1}, n_k..n_d), row-major to the DEVICE buffer
+ * out[(j-row0)*l + c].  kind 0 ignores dims (rtk_omega).  RTK_ERR_ARG on bad arguments or
+ * row0 + rows > prod_{j != mode} dims[j]; allocates its Khatri-Rao factor scratch with
+ * cudaMallocAsync on `stream`. */
+RTK_API int rtk_sketch(int32_t kind, uint64_t seed, int32_t mode, const int64_t* dims, int32_t d, int64_t row0,
+                       int64_t rows, int32_t l, float* out, void* stream);
 
 /* Test hook: one fused power step Y = M (M^T Q) on the column-major n x m matrix M (ld)
  * with Q (n x l, column-major, ld n; device, float32); Y (n x l, column-major fp64, device).

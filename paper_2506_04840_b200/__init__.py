@@ -19,8 +19,8 @@ n_k x r_k (column-major), core is r_1 x ... x r_d (column-major).
 from __future__ import annotations
 
 from ._lib import (ABI_FUNCTIONS, RtkError, as_column_major, lib_path, load_library, omega,
-                   power_step, profile_begin, profile_end, rthosvd, rsthosvd, rsthosvd_a2, solve,
+                   power_step, profile_begin, profile_end, rthosvd, rsthosvd, rsthosvd_a2, sketch, solve,
                    version, workspace_bytes)
 
-__all__ = ["rthosvd", "rsthosvd", "rsthosvd_a2", "solve", "omega", "power_step", "workspace_bytes",
+__all__ = ["rthosvd", "rsthosvd", "rsthosvd_a2", "solve", "sketch", "omega", "power_step", "workspace_bytes",
            "as_column_major", "RtkError", "profile_begin", "profile_end", "load_library", "lib_path", "version", "ABI_FUNCTIONS"]

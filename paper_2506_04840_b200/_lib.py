@@ -8,7 +8,8 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_omega",
+ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_workspace_bytes_ex",
+                 "rtk_omega", "rtk_sketch",
                  "rtk_power_step", "rtk_profile_begin", "rtk_profile_end", "rtk_debug_step_clocks",
                  "rtk_last_error", "rtk_version"]
 
@@ -37,7 +38,8 @@ class ProfStats(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("sequential", ctypes.c_int32), ("shift", ctypes.c_int32),
-                ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32), ("variant", ctypes.c_int32)]
+                ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("omega", ctypes.c_int32)]
 
 
 def lib_path() -> str:
@@ -68,6 +70,12 @@ def load_library():
     lib.rtk_workspace_bytes.argtypes = [ctypes.c_int32, i64p, ctypes.c_int32, i32p, ctypes.c_int32,
                                         ctypes.c_int32]
     lib.rtk_workspace_bytes.restype = ctypes.c_size_t
+    lib.rtk_workspace_bytes_ex.argtypes = [ctypes.POINTER(_Options), i64p, ctypes.c_int32, i32p, ctypes.c_int32,
+                                           ctypes.c_int32]
+    lib.rtk_workspace_bytes_ex.restype = ctypes.c_size_t
+    lib.rtk_sketch.argtypes = [ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32, i64p, ctypes.c_int32,
+                               ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+    lib.rtk_sketch.restype = ctypes.c_int
     lib.rtk_omega.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                               ctypes.c_int32, vp, vp]
     lib.rtk_omega.restype = ctypes.c_int
@@ -130,12 +138,14 @@ def _is_column_major(x) -> bool:
     return True
 
 
-def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int, variant: int = 0) -> int:
+def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int, variant: int = 0, omega_kind: int = 0,
+                    path: int = 0) -> int:
     lib = load_library()
     d = len(dims)
     dd = (ctypes.c_int64 * d)(*dims)
     rr = (ctypes.c_int32 * d)(*ranks)
-    n = lib.rtk_workspace_bytes(2 if variant == 1 else (1 if sequential else 0), dd, d, rr, p, q)
+    opt = _Options(1 if sequential else 0, 1, 0.0, int(path), int(variant), int(omega_kind))
+    n = lib.rtk_workspace_bytes_ex(ctypes.byref(opt), dd, d, rr, p, q)
     if n == 0:
         raise RtkError(1, lib.rtk_last_error().decode())
     return int(n)
@@ -172,12 +182,13 @@ _WS = _WorkspaceCache()
 
 def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: bool = True,
           report: bool = False, out=None, workspace=None, pve_tol: float = 0.0, path: int = 0,
-          variant: int = 0):
+          variant: int = 0, omega_kind: int = 0):
     """General solver: Alg. 4 (sequential) / Alg. 3 (not sequential); shift=False is Alg. 2.
 
     pve_tol > 0 selects Alg. B.1 (PAPER.md:1145-1172) with q as q_max (sequential only);
     path: 0 auto, 1 FP32 FFMA tiles, 2 tcgen05 3xTF32 (rtk_options.path).
     variant=1 selects Alg. A.2 (shift=False gives Alg. A.1).
+    omega_kind: 0 Gaussian, 1 uniform, 2 KR-Gaussian, 3 KR-uniform sketch.
 
     Returns (core, [U_1..U_d]) or (core, U, Report) with report=True.
     ``out=(core, [U_k])`` reuses caller-allocated outputs (column-major).
@@ -204,9 +215,10 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     dd = (ctypes.c_int64 * d)(*dims)
     rr = (ctypes.c_int32 * d)(*ranks)
     up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
-    ws_bytes = workspace_bytes(sequential, dims, ranks, p, q, variant) if min(ranks) >= 1 else 0
+    ws_bytes = workspace_bytes(sequential, dims, ranks, p, q, variant, omega_kind, path) if min(ranks) >= 1 else 0
     ws = workspace if workspace is not None else _WS.get(dev, max(ws_bytes, 1))
-    opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path), int(variant))
+    opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path), int(variant),
+                   int(omega_kind))
     rep = None
     bufs = None
     if report:
@@ -258,6 +270,25 @@ def omega(seed: int, mode: int, row0: int, rows: int, l: int, device="cuda"):
     with torch.cuda.device(out.device):
         _check(lib.rtk_omega(ctypes.c_uint64(seed), mode, row0, rows, l,
                              ctypes.c_void_p(out.data_ptr()), _stream_handle(out.device)))
+    return out
+
+
+def sketch(kind: int, seed: int, mode: int, dims, l: int, row0: int = 0, rows=None, device="cuda"):
+    """Rows [row0, row0+rows) of mode `mode`'s sketch of type `kind` (0 Gaussian, 1 uniform, 2/3
+    Khatri-Rao) for a tensor with extents `dims`, computed by the CUDA kernels (test hook)."""
+    import torch
+    lib = load_library()
+    d = len(dims)
+    m = 1
+    for j, n in enumerate(dims):
+        if j + 1 != mode:
+            m *= int(n)
+    rows = m - row0 if rows is None else rows
+    out = torch.empty((rows, l), dtype=torch.float32, device=device)
+    dd = (ctypes.c_int64 * d)(*[int(x) for x in dims])
+    with torch.cuda.device(out.device):
+        _check(lib.rtk_sketch(kind, ctypes.c_uint64(seed), mode, dd, d, row0, rows, l,
+                              ctypes.c_void_p(out.data_ptr()), _stream_handle(out.device)))
     return out
 
 

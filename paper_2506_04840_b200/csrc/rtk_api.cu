@@ -73,12 +73,21 @@ struct Problem {
   bool seq = true;
   double pve = 0.0;   // > 0: Alg. B.1 tolerance, q is q_max
   bool a2 = false;    // Alg. A.2: each mode keeps all l_k columns, then ST-HOSVD of the l-core
+  int omega = 0;      // sketch type: 0 RTK-GAUSS-1, 1 uniform, 2 KR-Gaussian, 3 KR-uniform
   std::vector<int> keep;   // columns kept by mode k's shrink: r_k, or l_k = r_k + p (A.2)
 };
 
 void set_keep(Problem& P) {
   P.keep.resize(P.d);
   for (int k = 0; k < P.d; ++k) P.keep[k] = P.ranks[k] + (P.a2 ? P.p : 0);
+}
+
+// extents of the tensor whose mode-k unfolding mode k factors (T: A; ST: the shrunk G)
+std::vector<int64_t> cur_dims(const Problem& P, int k) {
+  std::vector<int64_t> e(P.dims);
+  if (P.seq)
+    for (int j = 0; j < k; ++j) e[j] = P.keep[j];
+  return e;
 }
 
 // m_k: columns of the matrix mode k factors (PAPER.md:257 vs :300)
@@ -156,6 +165,7 @@ struct Layout {
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
   size_t g2part = 0, gsum = 0, amax = 0;
   size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
+  size_t om = 0, omtab = 0;                                         // Appendix D sketches only
   size_t shr_elems = 0;
   std::vector<TilePlan> sk, pw, sh;
 };
@@ -234,6 +244,17 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.amax = take((size_t)8 * 2 * kSolveLMax * 8);
   L.shr0 = take(shr * 4);
   L.shr1 = take(shr * 4);
+  if (P.omega) {
+    size_t oms = 0, tabs = 0;
+    for (int k = 0; k < P.d; ++k) {
+      const int l = P.ranks[k] + P.p;
+      oms = std::max(oms, (size_t)mode_cols(P, k) * l);
+      const std::vector<int64_t> e = cur_dims(P, k);
+      tabs = std::max(tabs, sketch_tab_floats(e.data(), P.d, k + 1, l));
+    }
+    L.om = take(oms * 4);
+    L.omtab = take(tabs * 4);
+  }
   if (P.a2) {
     size_t qa = 0, lt = 1;
     for (int k = 0; k < P.d; ++k) { qa += (size_t)P.dims[k] * P.keep[k]; lt *= (size_t)P.keep[k]; }
@@ -315,6 +336,15 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   const bool defer = fast && tc && P.q > 1 && !pve;   // deferred shift updates on the side stream
   if (defer) RTK_CK(side_streams(&side));
   bool pending = false;                       // an alpha_kernel is in flight on side->aux
+  const float* om = nullptr;   // Appendix D sketch types: Omega_k materialised once per mode
+  if (P.omega) {
+    const std::vector<int64_t> e = cur_dims(P, k);
+    ProfScope ps(0, k, st);
+    om = (const float*)(ws + L.om);
+    RTK_CK(sketch_materialize(P.omega, seed, k + 1, e.data(), P.d, 0, v.m(), l, (float*)(ws + L.omtab),
+                              (float*)(ws + L.om), st));
+    g_launches += 1 + (P.omega >= 2 ? P.d - 1 : 0);
+  }
   for (int step = 0; step <= P.q; ++step) {
     const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
     if (tc) {
@@ -329,13 +359,13 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         const bool sk = step == 0;
         RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
                            pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st, nullptr, 1, 1,
-                           1, sk ? nullptr : stop));
+                           1, sk ? nullptr : stop, om));
         g_launches += sk ? 1 : 0;
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
       } else {
       if (step == 0) {
-        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G, st));
+        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G, st, om));
         g_launches += 1;
       } else {
         if (!fast) RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));   // else: written by step_kernel
@@ -355,6 +385,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     T.qld = n;
     T.Ypart = B.Ypart;
     T.seed = seed;
+    T.om = om;
     T.mode = mode1;
     {
       ProfScope ps(step == 0 ? 0 : 1, k, st);
@@ -453,6 +484,9 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   P.dims.assign(dims, dims + d);
   P.ranks.assign(ranks, ranks + d);
   if (opt.variant < 0 || opt.variant > 1) return fail(RTK_ERR_ARG, "variant must be 0 (Alg. 2/3/4) or 1 (Alg. A.2)");
+  if (opt.omega < 0 || opt.omega > 3)
+    return fail(RTK_ERR_ARG, "omega must be 0 (Gaussian), 1 (uniform), 2 (KR-Gaussian) or 3 (KR-uniform)");
+  P.omega = opt.omega;
   P.a2 = opt.variant == 1;
   if (P.a2 && !P.seq) return fail(RTK_ERR_ARG, "Alg. A.2 is the sequential (ST-HOSVD) variant: set sequential = 1");
   if (P.a2 && opt.pve_tol > 0.0) return fail(RTK_ERR_ARG, "PVE (Alg. B.1) is stated for Alg. 4, not Alg. A.2");
@@ -569,7 +603,7 @@ extern "C" {
 int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
               int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws,
               size_t ws_bytes, void* stream, rtk_report* rep) {
-  rtk_options o = {1, 1, 0.0, 0, 0};
+  rtk_options o = {1, 1, 0.0, 0, 0, 0};
   if (opt) o = *opt;
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
@@ -577,14 +611,14 @@ int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32
 int rtk_rthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                 int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                 void* stream, rtk_report* rep) {
-  rtk_options o = {0, 1, 0.0, 0, 0};
+  rtk_options o = {0, 1, 0.0, 0, 0, 0};
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
 int rtk_rsthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                  int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                  void* stream, rtk_report* rep) {
-  rtk_options o = {1, 1, 0.0, 0, 0};
+  rtk_options o = {1, 1, 0.0, 0, 0, 0};
   return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
@@ -602,6 +636,47 @@ size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const i
   set_keep(P);
   if (validate(P)) return 0;
   return plan(P, num_sms(), nullptr, 0).total;
+}
+
+int rtk_sketch(int32_t kind, uint64_t seed, int32_t mode, const int64_t* dims, int32_t d, int64_t row0, int64_t rows,
+               int32_t l, float* out, void* stream) {
+  if (kind == 0) return rtk_omega(seed, mode, row0, rows, l, out, stream);
+  if (!out || !dims || d < 2 || d > 8 || mode < 1 || mode > d || rows < 0 || row0 < 0 || l < 1 || kind < 0 ||
+      kind > 3)
+    return fail(RTK_ERR_ARG, "invalid rtk_sketch arguments");
+  int64_t m = 1;
+  for (int j = 0; j < d; ++j) {
+    if (dims[j] < 1) return fail(RTK_ERR_ARG, "dims[k] must be >= 1");
+    if (j + 1 != mode) m *= dims[j];
+  }
+  if (row0 + rows > m) return fail(RTK_ERR_ARG, "rows past the unfolding's column count");
+  if (rows == 0) return RTK_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  float* tabs = nullptr;
+  const size_t tf = std::max<size_t>(sketch_tab_floats(dims, d, mode, l), 1);
+  RTK_CK(cudaMallocAsync((void**)&tabs, tf * 4, st));
+  RTK_CK(sketch_materialize(kind, seed, mode, dims, d, row0, rows, l, tabs, out, st));
+  RTK_CK(cudaFreeAsync(tabs, st));
+  return RTK_OK;
+}
+
+size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32_t d, const int32_t* ranks,
+                              int32_t p, int32_t q) {
+  rtk_options o = {1, 1, 0.0, 0, 0, 0};
+  if (opt) o = *opt;
+  if (!dims || !ranks || d < 2 || d > 8 || o.omega < 0 || o.omega > 3 || o.variant < 0 || o.variant > 1) {
+    g_err = "invalid arguments";
+    return 0;
+  }
+  Problem P;
+  P.d = d; P.p = p; P.q = q; P.seq = o.sequential != 0;
+  P.a2 = o.variant == 1;
+  P.omega = o.omega;
+  P.dims.assign(dims, dims + d);
+  P.ranks.assign(ranks, ranks + d);
+  set_keep(P);
+  if (validate(P)) return 0;
+  return plan(P, num_sms(), nullptr, o.path).total;
 }
 
 int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out, void* stream) {

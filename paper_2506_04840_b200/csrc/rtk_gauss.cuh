@@ -127,4 +127,20 @@ __device__ __forceinline__ float2 omega_pair(uint64_t seed, uint32_t mode, uint6
   return half ? box_muller(x.z, x.w) : box_muller(x.x, x.y);
 }
 
+// RTK-UNIF-1 value 2u - 1 = (2 (x >> 8) + 1 - 2^24) 2^-24, exact in binary32
+__device__ __forceinline__ float unif_sym(uint32_t x) {
+  return (float)((int)((x >> 8) << 1) + 1 - (1 << 24)) * 5.9604644775390625e-08f;
+}
+
+// Sketch columns (c2, c2 + 1) of row j (c2 even): from a materialised Omega_k ([m][l] row-major,
+// the Appendix D types, rtk_omega.cu) or RTK-GAUSS-1 generated in place (om == nullptr)
+__device__ __forceinline__ float2 sketch_pair(const float* om, int l, uint64_t seed, uint32_t mode, uint64_t j,
+                                              int c2) {
+  if (om) {
+    const float* p = om + j * (uint64_t)l + c2;
+    return make_float2(p[0], c2 + 1 < l ? p[1] : 0.f);
+  }
+  return omega_pair(seed, mode, j, (uint32_t)(c2 >> 2), (c2 >> 1) & 1);
+}
+
 }  // namespace rtk

@@ -48,6 +48,7 @@ struct TileLaunch {
   float* Ypart = nullptr;     // [G][ltot][n_rows]
   uint64_t seed = 0;
   uint32_t mode = 0;
+  const float* om = nullptr;  // SKETCH: materialised Omega_k [m][l] (Appendix D types) or nullptr
   float* out = nullptr;       // SHRINK destination
   int64_t Rprev = 1, nnext = 1, ldnext = 1;
 };
@@ -114,7 +115,7 @@ cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* p
 cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,
                    int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st, int max_ctas = 0);
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
-                   float* Ypart, int G, cudaStream_t st);
+                   float* Ypart, int G, cudaStream_t st, const float* om = nullptr);
 
 // ---- fused single-pass power step (rtk_fused.cu) -----------------------------------
 int fused_cluster(int n);
@@ -123,6 +124,14 @@ size_t fused_ypart_floats(const View& v, int l, int grid);
 cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
                         uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st,
                         float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1,
-                        const int* stop = nullptr);
+                        const int* stop = nullptr, const float* om = nullptr);
+
+// ---- Appendix D sketch types (rtk_omega.cu) ------------------------------------------
+// Materialise Omega_k rows [row0, row0 + rows) x l (row-major [j][l]) of the given type for the
+// mode-mode1 unfolding of a tensor with extents dims[0..d-1]; tabs: scratch for the Khatri-Rao
+// factors (sum_{m != k} dims[m] * l floats).  kind: 1 uniform, 2 KR-Gaussian, 3 KR-uniform.
+cudaError_t sketch_materialize(int kind, uint64_t seed, int mode1, const int64_t* dims, int d, int64_t row0,
+                               int64_t rows, int l, float* tabs, float* out, cudaStream_t st);
+size_t sketch_tab_floats(const int64_t* dims, int d, int mode1, int l);
 
 }  // namespace rtk

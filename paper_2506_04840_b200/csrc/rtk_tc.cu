@@ -58,6 +58,7 @@ struct TcOp2Args {
   int sketch;
   uint64_t seed;
   uint32_t mode;
+  const float* om;   // materialised Omega_k [m][l] or nullptr (RTK-GAUSS-1 in place)
 };
 
 // ------------------------------------------------------------------ op1: W = M^T Q
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
           const int jj = it2 % kBK, c2 = (it2 / kBK) * 2;
           const int64_t j = kc * kBK + jj;
           float2 z = make_float2(0.f, 0.f);
-          if (j < a.m && c2 < a.l) z = omega_pair(a.seed, a.mode, (uint64_t)j, c2 >> 2, (c2 >> 1) & 1);
+          if (j < a.m && c2 < a.l) z = sketch_pair(a.om, a.l, a.seed, a.mode, (uint64_t)j, c2);
           const float z1 = (c2 + 1 < a.l) ? z.y : 0.f;
           const float h0 = tf32_rna(z.x), h1 = tf32_rna(z1);
           *reinterpret_cast<float*>(bt + sw128_offset(c2, jj)) = h0;
@@ -510,7 +511,7 @@ cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t 
 
 // op2: Ypart[G][N][nit*128] = per-CTA partial M W (or M Omega_k when sketch)
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
-                   float* Ypart, int G, cudaStream_t st) {
+                   float* Ypart, int G, cudaStream_t st, const float* om) {
   const int N = tc_npad(l);
   CUtensorMap mM, mB;
   if (!make_map(&mM, v.base, (uint64_t)v.n, (uint64_t)v.m(), (uint64_t)v.ss, 32, 32,
@@ -523,7 +524,7 @@ cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketc
   }
   TcOp2Args a;
   a.n = v.n; a.N = N; a.l = l; a.m = v.m(); a.nit = (v.n + 127) / 128; a.nkc = (v.m() + kBK - 1) / kBK;
-  a.G = G; a.Ypart = Ypart; a.sketch = sketch ? 1 : 0; a.seed = seed; a.mode = mode;
+  a.G = G; a.Ypart = Ypart; a.sketch = sketch ? 1 : 0; a.seed = seed; a.mode = mode; a.om = om;
   switch (N) {
     case 16: return op2_launch<16>(mM, mB, a, G, st);
     case 32: return op2_launch<32>(mM, mB, a, G, st);

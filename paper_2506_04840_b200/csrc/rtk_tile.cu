@@ -45,6 +45,7 @@ struct TileArgs {
   int64_t yp_g;  // ltot * n_rows
   uint64_t seed;
   uint32_t mode;
+  const float* om;   // materialised Omega_k [m][l] (Appendix D types) or nullptr (RTK-GAUSS-1)
   float* out;
   int64_t Rprev, nnext, ldnext;
 };
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256) tile_kernel(const TileArgs a) {
         const int cgl = chunk * a.LC + c2;             // global sketch column (even)
         const int64_t jg = j0 + j;
         float2 z = make_float2(0.f, 0.f);
-        if (jg < a.m && cgl < a.l) z = omega_pair(a.seed, a.mode, (uint64_t)jg, cgl >> 2, (cgl >> 1) & 1);
+        if (jg < a.m && cgl < a.l) z = sketch_pair(a.om, a.l, a.seed, a.mode, (uint64_t)jg, cgl);
         Wsm[j * a.LC + c2] = z.x;
         Wsm[j * a.LC + c2 + 1] = (cgl + 1 < a.l) ? z.y : 0.f;
       }
@@ -487,7 +488,7 @@ cudaError_t launch_tile(const TileLaunch& L, cudaStream_t st) {
   a.n_rows = p.n_rows(); a.pitch = p.pitch; a.NRG = p.NRG; a.LC = p.LC;
   a.nchunks = p.nchunks; a.G = p.G; a.b = p.b; a.ntiles = p.ntiles; a.l = L.l;
   a.Q = L.Q; a.qld = L.qld; a.Ypart = L.Ypart; a.yp_g = (int64_t)p.ltot() * p.n_rows();
-  a.seed = L.seed; a.mode = L.mode; a.out = L.out; a.Rprev = L.Rprev; a.nnext = L.nnext;
+  a.seed = L.seed; a.mode = L.mode; a.om = L.om; a.out = L.out; a.Rprev = L.Rprev; a.nnext = L.nnext;
   a.ldnext = L.ldnext;
   const int grid = p.G * p.nchunks;
   const size_t smem = tile_smem(p.b, p.pitch, p.LC, p.NT);

@@ -1,6 +1,7 @@
 """One profiled solve of a config through the public API; prints device ms by (kind, mode).
 
-python scripts/prof_solve.py [c5] [reps] [a2]   (a2: Alg. A.2 instead of the config's algorithm)
+python scripts/prof_solve.py [c5] [reps] [a2|-] [omega_kind]
+  a2: Alg. A.2 instead of the config's algorithm; omega_kind: 0 Gaussian, 1 uniform, 2/3 Khatri-Rao
 """
 import json
 import os
@@ -23,6 +24,10 @@ def main():
     fn = rt.rsthosvd if c["algo"] == "rsthosvd" else rt.rthosvd
     if len(sys.argv) > 3 and sys.argv[3] == "a2":
         fn, name = rt.rsthosvd_a2, name + "-a2"
+    kind = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    if kind:
+        import functools
+        fn, name = functools.partial(fn, omega_kind=kind), name + f"-omega{kind}"
     fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"])
     torch.cuda.synchronize()
     rt.profile_begin()

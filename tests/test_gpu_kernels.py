@@ -86,3 +86,21 @@ def test_power_step_padded_leading_dimension():
     M = buf[:n].astype(np.float64)
     ref = M @ (M.T @ Q.astype(np.float64))
     assert np.linalg.norm(Y - ref) / np.linalg.norm(ref) < 2e-6
+
+
+# ------------------------------------------------ Appendix D sketch types
+@pytest.mark.parametrize("kind", [1, 2, 3])
+@pytest.mark.parametrize("dims,mode,l,row0,rows", [
+    ((30, 20, 10), 1, 13, 0, None),
+    ((30, 20, 10), 2, 16, 7, 101),
+    ((9, 8, 7, 6), 3, 21, 0, None),
+    ((5, 4), 2, 3, 1, 3),
+])
+def test_sketch_types_bit_exact(kind, dims, mode, l, row0, rows):
+    """The CUDA RTK-UNIF-1 / RTK-KR-1 generators equal the oracle's bit for bit."""
+    torch = cuda_or_skip()
+    from oracle import gauss
+    from paper_2506_04840_b200 import sketch
+    got = sketch(kind, 0xABCDEF0123, mode, dims, l, row0, rows).cpu().numpy()
+    ref = gauss.sketch(kind, 0xABCDEF0123, mode, dims, l, row0, rows)
+    np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32))

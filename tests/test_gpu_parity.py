@@ -291,3 +291,38 @@ def test_a2_rejected_where_undefined():
         solve(A, (3, 3, 3), 2, 2, 1, sequential=False, variant=1)     # A.2 is ST only
     with pytest.raises(Exception):
         solve(A, (3, 3, 3), 2, 2, 1, sequential=True, variant=1, pve_tol=0.1)
+
+
+# ------------------------------------------------------------ Appendix D sketch types
+@pytest.mark.parametrize("kind", [1, 2, 3])
+@pytest.mark.parametrize("algo", ["t", "st", "a2"])
+@pytest.mark.parametrize("path", ["ffma", "fused"])
+def test_sketch_type_parity(kind, algo, path, monkeypatch):
+    """Uniform / KR-Gaussian / KR-uniform sketches through every algorithm and streaming path."""
+    monkeypatch.setenv("RTK_PATH", "ffma" if path == "ffma" else "tc")
+    monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import solve
+    rng = np.random.default_rng(60 + kind)
+    dims, ranks, p, q = (96, 40, 36), (12, 6, 5), 4, 2
+    cr = (16, 10, 9)
+    core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    A = to_device_colmajor(a, torch)
+    seq, variant = algo != "t", 1 if algo == "a2" else 0
+    g_core, g_U, rep = solve(A, ranks, p, q, 17, sequential=seq, variant=variant, omega_kind=kind, report=True)
+    torch.cuda.synchronize()
+    fn = {"t": tucker.rthosvd, "st": tucker.rsthosvd, "a2": tucker.rsthosvd_a2}[algo]
+    orc = fn(a, ranks, p, q, 17, omega_kind=kind)
+    g_core, g_U = g_core.cpu().numpy(), [u.cpu().numpy() for u in g_U]
+    re_g = metrics.relative_error(a, g_core, g_U)
+    re_o = metrics.relative_error(a, orc.core, orc.factors)
+    assert abs(re_g - re_o) <= RE_TOL * re_o + 1e-7, (re_g, re_o)
+    gaps = metrics.mode_gaps(a, ranks, orc.factors, seq)
+    for k, u in enumerate(g_U):
+        assert metrics.orthonormality(u) <= ORTH_TOL
+        if gaps[k] > 0.10:
+            assert metrics.max_principal_angle(orc.factors[k], u) <= ANGLE_TOL
+    for k, tr in enumerate(orc.traces):
+        if tr.alpha and max(tr.alpha) > 0:
+            np.testing.assert_allclose(rep.alpha_trace[k], tr.alpha, rtol=5e-3, atol=1e-12)
