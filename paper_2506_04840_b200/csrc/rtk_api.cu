@@ -59,7 +59,6 @@ int fail(int code, const std::string& msg) {
 
 constexpr int kLMaxApi = 96;
 constexpr int kNMax = 4096;
-constexpr int kRB = 16;
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

@@ -817,10 +817,12 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   bool two_pass = false;
   if (!eig) {
     const bool ok = chol_upper(S.G, S.R, S.rowbuf, l);
+    tck[ntck++] = clock64();
     if (!ok) {
       eig = true;
     } else {
       tri_inv_upper(S.R, S.T, l, S.lam);
+      tck[ntck++] = clock64();
       // kappa_F(R) = ||R||_F ||R^{-1}||_F >= kappa_2(Y); one CholQR pass leaves
       // ||Q^T Q - I|| ~ eps kappa^2
       if (tid < 32) {
