@@ -326,3 +326,37 @@ def test_sketch_type_parity(kind, algo, path, monkeypatch):
     for k, tr in enumerate(orc.traces):
         if tr.alpha and max(tr.alpha) > 0:
             np.testing.assert_allclose(rep.alpha_trace[k], tr.alpha, rtol=5e-3, atol=1e-12)
+
+
+# ------------------------------------------------------------ edge cases and limits
+@pytest.mark.parametrize("seq", [False, True])
+@pytest.mark.parametrize("dims,ranks,p,q", [
+    ((8, 30, 20), (6, 4, 3), 2, 2),            # l_1 = n_1: the sketch spans the whole mode
+    ((12, 10, 9), (12, 3, 2), 0, 1),           # r_1 = n_1, p = 0 (l = r)
+    ((1, 30, 20), (1, 4, 3), 0, 2),            # n_1 = 1 (a matrix in disguise)
+    ((300, 90, 90), (70, 8, 6), 10, 2),        # l_1 = 80 > 64: the one-CTA Jacobi small solves
+    ((4096, 9, 7), (6, 3, 2), 3, 1),           # n_k at the kernel limit (4096)
+])
+def test_edge_shapes(seq, dims, ranks, p, q):
+    rng = np.random.default_rng(sum(dims) + 3)
+    cr = tuple(min(n, r + 3) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) * np.exp(-0.25 * np.indices(cr).sum(axis=0))
+    us = [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)]
+    a = tucker_tensor(core, us, noise=1e-3, rng=rng)
+    check(a, ranks, p, q, 91, seq, alpha_rtol=5e-3)
+
+
+@pytest.mark.parametrize("seq", [False, True])
+def test_zero_tensor(seq):
+    """All-zero input (rank 0 < l): no shift update, the null basis is completed by the Philox
+    block, U orthonormal and finite, core exactly zero."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import solve
+    A = to_device_colmajor(np.zeros((20, 16, 12), dtype=np.float32), torch)
+    core, U, rep = solve(A, (3, 3, 2), 2, 2, 5, sequential=seq, report=True)
+    torch.cuda.synchronize()
+    assert all(x == 0.0 for t in rep.alpha_trace for x in t)
+    assert torch.count_nonzero(core).item() == 0
+    for u in U:
+        un = u.cpu().numpy()
+        assert np.all(np.isfinite(un)) and metrics.orthonormality(un) <= ORTH_TOL
