@@ -10,7 +10,7 @@
 //       G = sum_b Gram_b                        (cluster-parallel sum, fixed order)
 //       every CTA redundantly (identical inputs -> identical results) factors the l x l G:
 //         span path   (sketch / non-final power step):  G = R^T R, T = R^{-1};
-//                      a second CholQR pass only if eps * kappa_F(R)^2 > 1e-10
+//                      a second CholQR pass only if eps * kappa_F(R)^2 > 1e-7 (C20)
 //         shift       (power steps): Sigma_ll = sqrt(lambda_min(G)) by Householder
 //                      tridiagonalisation + Sturm multisection; alpha <- (Sigma_ll + alpha)/2
 //                      if Sigma_ll > alpha (degenerate guard SPEC.md:347)
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
           rf += __shfl_xor_sync(0xffffffffu, rf, o);
           tf += __shfl_xor_sync(0xffffffffu, tf, o);
         }
-        if (tid == 0) S.flags[0] = (DBL_EPSILON * rf * tf > 1e-10) ? 1 : 0;
+        if (tid == 0) S.flags[0] = (DBL_EPSILON * rf * tf > 1e-7) ? 1 : 0;
       }
       __syncthreads();
       two_pass = S.flags[0] != 0;
