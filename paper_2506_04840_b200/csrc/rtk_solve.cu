@@ -64,27 +64,56 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
                                                          double* __restrict__ Y, double* __restrict__ gpart,
                                                          const int* __restrict__ stop) {
   __shared__ double Ys[kRBr][kSL + 1];
+  __shared__ double red[4][kSL][kRBr];
   if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kRBr;
   const int rows = min(kRBr, n - i0);
   const double a = power ? *alpha : 0.0;
   const int64_t gs = (int64_t)ltot * n_rows;
+  static_assert(kRBr == 8 && kST == 4 * kSL, "thread (column c, partial slice h) layout");
+  {   // thread (c, h) sums the partials g = h, h+4, ... of its column's 8 rows: two 16-B loads
+      // per partial, all independent (the rows past n are Ypart padding, masked below)
+    const int c = tid % kSL, h = tid / kSL;
+    double acc[kRBr];
+#pragma unroll
+    for (int ii = 0; ii < kRBr; ++ii) acc[ii] = 0.0;
+    if (c < l) {
+      const float* src = Ypart + (int64_t)c * n_rows + i0;
+      int g = h;
+      for (; g + 12 < G; g += 16) {   // 4 partials of this slice in flight
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4* p = reinterpret_cast<const float4*>(src + (int64_t)(g + 4 * u) * gs);
+          v[2 * u] = __ldcg(p);
+          v[2 * u + 1] = __ldcg(p + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[0] += (double)v[2 * u].x; acc[1] += (double)v[2 * u].y;
+          acc[2] += (double)v[2 * u].z; acc[3] += (double)v[2 * u].w;
+          acc[4] += (double)v[2 * u + 1].x; acc[5] += (double)v[2 * u + 1].y;
+          acc[6] += (double)v[2 * u + 1].z; acc[7] += (double)v[2 * u + 1].w;
+        }
+      }
+      for (; g < G; g += 4) {
+        const float4* p = reinterpret_cast<const float4*>(src + (int64_t)g * gs);
+        const float4 x = __ldcg(p), y = __ldcg(p + 1);
+        acc[0] += (double)x.x; acc[1] += (double)x.y; acc[2] += (double)x.z; acc[3] += (double)x.w;
+        acc[4] += (double)y.x; acc[5] += (double)y.y; acc[6] += (double)y.z; acc[7] += (double)y.w;
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < kRBr; ++ii) red[h][c][ii] = acc[ii];
+  }
+  __syncthreads();
   for (int idx = tid; idx < kRBr * l; idx += kST) {
     const int c = idx / kRBr, ii = idx % kRBr;
     double s = 0.0;
-    if (ii < rows) {
+    if (ii < rows) {   // the four slices in a fixed order: repeatable results
       const int i = i0 + ii;
-      const float* src = Ypart + (int64_t)c * n_rows + i;
-      int g = 0;
-      for (; g + 8 <= G; g += 8) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(g + u) * gs);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += (double)v[u];
-      }
-      for (; g < G; ++g) s += (double)__ldcg(src + (int64_t)g * gs);
+      s = ((red[0][c][ii] + red[1][c][ii]) + red[2][c][ii]) + red[3][c][ii];
       if (power) s -= a * Qd[(int64_t)c * n + i];
       Y[(int64_t)c * n + i] = s;
     }
