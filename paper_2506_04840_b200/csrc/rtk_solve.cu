@@ -890,7 +890,6 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     }
   }
   if (eig) {
-    two_pass = true;
     tck[ntck++] = clock64();
     if (!have_eigs) {   // tridiag / all_eigs results are still intact when B.1 computed them
       tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
@@ -923,7 +922,17 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       const int k = idx / kSL, cc = idx % kSL;
       S.T[k * kMLD + cc] = (k < l && cc < l) ? Z[k * kLD + (l - 1 - cc)] * S.colscale[cc] : 0.0;
     }
+    // second CholQR pass when one pass cannot leave ||Q^T Q - I|| <~ 1e-7 (C20): completed null
+    // columns, eps kappa(Y)^2 = eps lambda_max / lambda_min > 1e-7, or eigenvalues so close
+    // (relative gap < 1e-8) that inverse iteration may return non-orthogonal vectors
+    if (tid == 0) {
+      bool tp = S.flags[1] != 0 || !(DBL_EPSILON * S.lam[l - 1] <= 1e-7 * S.lam[0]);
+      for (int k = 0; k + 1 < l && !tp; ++k)
+        if (S.lam[k + 1] - S.lam[k] < 1e-8 * S.lam[l - 1]) tp = true;
+      S.flags[3] = tp ? 1 : 0;
+    }
     __syncthreads();
+    two_pass = S.flags[3] != 0;
     lam_min = fmax(S.lam[0], 0.0);
     s1 = sg1;
   }
