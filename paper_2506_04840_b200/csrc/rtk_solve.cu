@@ -73,12 +73,17 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
   const int64_t gs = (int64_t)ltot * n_rows;
   static_assert(kRBr == 8 && kST == 4 * kSL, "thread (column c, partial slice h) layout");
   {   // thread (c, h) sums the partials g = h, h+4, ... of its column's 8 rows: two 16-B loads
-      // per partial, all independent (the rows past n are Ypart padding, masked below)
+      // per partial, all independent (the rows past n are Ypart padding, masked below; n_rows is a
+      // multiple of 4, and a last group with only 4 rows inside n_rows takes the scalar loop)
     const int c = tid % kSL, h = tid / kSL;
     double acc[kRBr];
 #pragma unroll
     for (int ii = 0; ii < kRBr; ++ii) acc[ii] = 0.0;
-    if (c < l) {
+    if (c < l && i0 + kRBr > n_rows) {
+      const float* src = Ypart + (int64_t)c * n_rows + i0;
+      for (int g = h; g < G; g += 4)
+        for (int ii = 0; ii < n_rows - i0; ++ii) acc[ii] += (double)__ldcg(src + (int64_t)g * gs + ii);
+    } else if (c < l) {
       const float* src = Ypart + (int64_t)c * n_rows + i0;
       int g = h;
       for (; g + 12 < G; g += 16) {   // 4 partials of this slice in flight

@@ -405,10 +405,8 @@ static bool valid_combo(int R, int TC, int NCG) {
 
 static void finish_plan(TilePlan& p, int n, int l, int nsm) {
   const int NRG = (n + p.R - 1) / p.R;
-  // padded row groups (extra rows are zero); a multiple of 8 so that n_rows is too (the reduce
-  // reads 8-row groups of every partial with 16-B loads)
-  const int lanes = std::max(32 / p.NCG, 8);
-  p.NRG = (NRG + lanes - 1) / lanes * lanes;
+  const int lanes = 32 / p.NCG;
+  p.NRG = (NRG + lanes - 1) / lanes * lanes;   // padded row groups (extra rows are zero)
   p.NT = p.NRG * p.NCG;
   p.LC = p.NCG * p.TC;
   p.nchunks = (l + p.LC - 1) / p.LC;
