@@ -568,7 +568,9 @@ __device__ void all_eigs(const double* d, const double* e, const double* e2, int
       }
       blo[c] = lo;
       bhi[c] = hi;
-      done = (hi - lo) <= 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300;
+      // converged: 1e-15 relative, or the 4 eps ||T|| absolute accuracy a Sturm count can resolve
+      // at all (without it tiny eigenvalues ran the full 40 rounds)
+      done = (hi - lo) <= fmax(1e-15 * fmax(fabs(lo), fabs(hi)), 4.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu))) + 1e-300;
     }
     if (__syncthreads_and(done)) break;
   }
