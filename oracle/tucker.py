@@ -65,6 +65,15 @@ def econ_svd(y: np.ndarray):
     return q, s
 
 
+def leading_left_vectors(m: np.ndarray, r: int) -> np.ndarray:
+    """First r left singular vectors of m (n x c), r <= n: from the economy SVD when r <= c, else
+    from the full SVD (the last r - c columns then span part of the null space of m^T, any
+    orthonormal completion being equally valid; Alg. 1 line "U_k = first r_k left singular
+    vectors", PAPER.md:113-125, is defined for r_k <= n_k whatever the column count)."""
+    q, _, _ = np.linalg.svd(m, full_matrices=r > m.shape[1])
+    return q[:, :r]
+
+
 # ----------------------------------------------------------------- Algorithm 1
 def thosvd(a: np.ndarray, ranks, sequential: bool):
     """Deterministic T-HOSVD / ST-HOSVD, Alg. 1.
@@ -77,8 +86,7 @@ def thosvd(a: np.ndarray, ranks, sequential: bool):
     us = []
     for k, r in enumerate(ranks):
         m = unfold(g if sequential else a64, k)
-        q, _ = econ_svd(m)
-        u = sign_pin(q[:, :r])
+        u = sign_pin(leading_left_vectors(m, r))
         us.append(u)
         g = mode_product(g, u.T, k)
     return g, us
@@ -223,8 +231,7 @@ def rsthosvd_a2(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = T
     g = b
     us = []
     for k, r in enumerate(ranks):                                                      # line 14
-        v, _ = econ_svd(unfold(g, k))
-        v = v[:, :r]
+        v = leading_left_vectors(unfold(g, k), r)
         u = qs[k] @ v                                                                  # line 15
         u_p = sign_pin(u)
         sgn = np.where(np.sum(u_p * u, axis=0) < 0.0, -1.0, 1.0)

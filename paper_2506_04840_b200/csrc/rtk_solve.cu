@@ -1271,30 +1271,40 @@ __global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict
   }
   __syncthreads();
   for (int cc = 0; cc < r; ++cc) {
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int jj = warp; jj < cc; jj += kST / 32) {   // dots with the finished columns
+    // the eigenvector first; if Gram-Schmidt leaves (almost) nothing of it -- a duplicate from a
+    // degenerate cluster, e.g. the null space when r_k exceeds the rank of the l-core's unfolding --
+    // complete with the first unit vector e_i that keeps a quarter of its norm
+    for (int attempt = 0; attempt <= c; ++attempt) {
+      if (attempt > 0) {
+        if (tid < c) S.R[tid * kLD + cc] = (tid == attempt - 1) ? 1.0 : 0.0;
+        __syncthreads();
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int jj = warp; jj < cc; jj += kST / 32) {   // dots with the finished columns
+          double t = 0.0;
+          for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + jj], S.R[i * kLD + cc], t);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+          if (lane == 0) S.dots[jj] = t;
+        }
+        __syncthreads();
+        if (tid < c) {
+          double x = S.R[tid * kLD + cc];
+          for (int jj = 0; jj < cc; ++jj) x = fma(-S.dots[jj], S.R[tid * kLD + jj], x);
+          S.R[tid * kLD + cc] = x;
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {
         double t = 0.0;
-        for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + jj], S.R[i * kLD + cc], t);
+        for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + cc], S.R[i * kLD + cc], t);
 #pragma unroll
         for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) S.dots[jj] = t;
+        if (lane == 0) { S.dbuf[1] = t; S.dbuf[0] = t > 0.0 ? 1.0 / sqrt(t) : 0.0; }
       }
       __syncthreads();
-      if (tid < c) {
-        double x = S.R[tid * kLD + cc];
-        for (int jj = 0; jj < cc; ++jj) x = fma(-S.dots[jj], S.R[tid * kLD + jj], x);
-        S.R[tid * kLD + cc] = x;
-      }
-      __syncthreads();
+      if (S.dbuf[1] >= (attempt == 0 ? 1e-4 : 0.25)) break;
     }
-    if (warp == 0) {
-      double t = 0.0;
-      for (int i = lane; i < c; i += 32) t = fma(S.R[i * kLD + cc], S.R[i * kLD + cc], t);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) S.dbuf[0] = t > 0.0 ? 1.0 / sqrt(t) : 0.0;
-    }
-    __syncthreads();
     if (tid < c) S.R[tid * kLD + cc] *= S.dbuf[0];
     __syncthreads();
   }

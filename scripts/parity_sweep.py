@@ -1,0 +1,107 @@
+"""Randomised GPU-vs-oracle parity sweep (robustness, not a unit test): random shapes, ranks, p, q,
+algorithm (Alg. 3 / 4 / A.2), streaming path, shift on/off and sketch type, each checked with the
+north_star tolerances.  Prints one line per case and a summary; exits 1 on any failure.
+
+python scripts/parity_sweep.py [n_cases] [seed]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2506_04840_b200 as rt  # noqa: E402
+from oracle import metrics, tucker  # noqa: E402
+from workloads import orthonormal_factor, tucker_tensor  # noqa: E402
+
+
+def case(rng):
+    d = int(rng.integers(2, 5))
+    budget = {2: 400000, 3: 2000000, 4: 1500000}[d]
+    while True:
+        dims = [int(rng.integers(2, 700 if d == 2 else (220 if d == 3 else 48))) for _ in range(d)]
+        if int(np.prod(dims)) <= budget:
+            break
+    algo = ["t", "st", "a2"][int(rng.integers(0, 3))] if d > 1 else "st"
+    p = int(rng.integers(0, 11))
+    ranks = []
+    for k, n in enumerate(dims):
+        ranks.append(int(rng.integers(1, max(2, min(n, 40)))))
+    # respect l_k <= min(n_k, m_k) (m_k over the shrunk extents for ST / A.2)
+    for _ in range(50):
+        ok = True
+        keep = []
+        for k, n in enumerate(dims):
+            l = ranks[k] + p
+            m = 1
+            for j, nj in enumerate(dims):
+                if j == k:
+                    continue
+                if algo != "t" and j < k:
+                    m *= keep[j]
+                else:
+                    m *= nj
+            if l > n or l > m or l > (64 if algo == "a2" else 96):
+                ok = False
+                if p > 0:
+                    p -= 1
+                else:
+                    ranks[k] = max(1, ranks[k] // 2)
+                break
+            keep.append(ranks[k] + (p if algo == "a2" else 0))
+        if ok:
+            break
+    else:
+        return None
+    q = int(rng.integers(1, 5))
+    path = ["ffma", "tc"][int(rng.integers(0, 2))]
+    shift = bool(rng.integers(0, 4) > 0)
+    omega = int(rng.integers(0, 4)) if rng.integers(0, 3) == 0 else 0
+    return dict(dims=dims, ranks=ranks, p=p, q=q, algo=algo, path=path, shift=shift, omega=omega)
+
+
+def main():
+    n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+    fails = 0
+    done = 0
+    while done < n_cases:
+        c = case(rng)
+        if c is None:
+            continue
+        done += 1
+        dims, ranks = c["dims"], c["ranks"]
+        cr = [min(n, r + 3) for n, r in zip(dims, ranks)]
+        core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
+        a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+        os.environ["RTK_PATH"] = c["path"]
+        A = torch.from_numpy(np.asfortranarray(a)).cuda()
+        seq, variant = c["algo"] != "t", 1 if c["algo"] == "a2" else 0
+        try:
+            g_core, g_U = rt.solve(A, ranks, c["p"], c["q"], 5, sequential=seq, variant=variant, shift=c["shift"],
+                                   omega_kind=c["omega"])
+            torch.cuda.synchronize()
+        except Exception as e:   # noqa: BLE001
+            print("ERROR", c, e, flush=True)
+            fails += 1
+            continue
+        fn = {"t": tucker.rthosvd, "st": tucker.rsthosvd, "a2": tucker.rsthosvd_a2}[c["algo"]]
+        orc = fn(a, ranks, c["p"], c["q"], 5, shift=c["shift"], omega_kind=c["omega"])
+        gU = [u.cpu().numpy() for u in g_U]
+        re_g = metrics.relative_error(a, g_core.cpu().numpy(), gU)
+        re_o = metrics.relative_error(a, orc.core, orc.factors)
+        gaps = metrics.mode_gaps(a, ranks, orc.factors, seq)
+        orth = max(metrics.orthonormality(u) for u in gU)
+        ang = max([metrics.max_principal_angle(uo, ug) for uo, ug, gp in zip(orc.factors, gU, gaps) if gp > 0.1]
+                  or [0.0])
+        ok = abs(re_g - re_o) <= 1e-4 * re_o + 1e-7 and orth <= 1e-5 and ang <= 1e-3
+        fails += 0 if ok else 1
+        print(("ok  " if ok else "FAIL"), c, f"RE {re_g:.6e}/{re_o:.6e} orth {orth:.1e} angle {ang:.1e}", flush=True)
+    print(f"{done - fails}/{done} cases within tolerance")
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -360,3 +360,22 @@ def test_zero_tensor(seq):
     for u in U:
         un = u.cpu().numpy()
         assert np.all(np.isfinite(un)) and metrics.orthonormality(un) <= ORTH_TOL
+
+
+def test_a2_rank_exceeds_core_rank():
+    """d = 2 with r_1 = 38 > rank of the 39 x 7 l-core's mode-1 unfolding: lines 14-15 must still
+    return an orthonormal U_1 (null-space completion; parity sweep case)."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import rsthosvd_a2
+    rng = np.random.default_rng(77)
+    a = tucker_tensor(rng.standard_normal((41, 9)) * np.exp(-0.2 * np.indices((41, 9)).sum(axis=0)),
+                      [orthonormal_factor(474, 41, rng), orthonormal_factor(400, 9, rng)], noise=1e-3, rng=rng)
+    A = to_device_colmajor(a, torch)
+    core, U = rsthosvd_a2(A, (38, 6), 1, 1, 5)
+    orc = tucker.rsthosvd_a2(a, (38, 6), 1, 1, 5)
+    gU = [u.cpu().numpy() for u in U]
+    for u in gU:
+        assert metrics.orthonormality(u) <= ORTH_TOL
+    re_g = metrics.relative_error(a, core.cpu().numpy(), gU)
+    re_o = metrics.relative_error(a, orc.core, orc.factors)
+    assert abs(re_g - re_o) <= RE_TOL * re_o

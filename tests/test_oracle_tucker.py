@@ -460,3 +460,19 @@ def test_kr_sketch_tensor_b_closed_form(kind):
     res = tucker.rsthosvd(a, (r, r, r), 5, 2, 3, omega_kind=kind)
     re = metrics.relative_error(a, res.core, res.factors)
     assert cf * (1 - 1e-12) <= re <= cf * (1 + 1e-3), (re, cf)
+
+
+def test_a2_rank_above_unfolding_columns():
+    """Alg. A.2 with p = 0 on a matrix, r_1 = 5 > the 4 columns of the l-core's mode-1 unfolding:
+    U_1 keeps r_1 orthonormal columns spanning span(Q_1) and the core identity still holds."""
+    rng = np.random.default_rng(45)
+    a = rng.standard_normal((34, 8)) @ rng.standard_normal((8, 60))
+    res = tucker.rsthosvd_a2(a, (5, 4), 0, 1, 5)
+    assert res.factors[0].shape == (34, 5)
+    assert metrics.orthonormality(res.factors[0]) <= 1e-12
+    q1, _ = tucker._range_finder(tucker.unfold(a, 0), 5, 0, 1, 5, 1, True, full=True)
+    assert metrics.max_principal_angle(q1, res.factors[0]) <= 1e-10
+    g = a
+    for k, u in enumerate(res.factors):
+        g = tucker.mode_product(g, u.T, k)
+    np.testing.assert_allclose(res.core, g, atol=1e-10)
