@@ -49,11 +49,18 @@ def reconstruct(core: np.ndarray, factors) -> np.ndarray:
     return t
 
 
+PIN_TIE = 1e-5
+
+
 def sign_pin(u: np.ndarray) -> np.ndarray:
     """SPEC.md:232 sign convention: each column's
-    largest-|entry| made positive, lowest row index on ties."""
+    largest-|entry| made positive, lowest row index on ties, where entries within
+    PIN_TIE (relative) of the column's largest |entry| count as tied (C6:
+    fp32 data cannot order closer magnitudes, and an unstable pick flips a column)."""
     u = np.array(u, dtype=np.float64, copy=True)
-    idx = np.argmax(np.abs(u), axis=0)
+    a = np.abs(u)
+    cand = a >= (1.0 - PIN_TIE) * a.max(axis=0)[None, :]
+    idx = np.argmax(cand, axis=0)                  # first (lowest) qualifying row
     s = np.sign(u[idx, np.arange(u.shape[1])])
     s[s == 0] = 1.0
     return u * s[None, :]

@@ -240,7 +240,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.sighat = take(lmax * 8);
   L.g2part = take((size_t)8 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
-  L.amax = take((size_t)8 * 2 * kSolveLMax * 8);
+  L.amax = take((size_t)8 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices
   L.shr0 = take(shr * 4);
   L.shr1 = take(shr * 4);
   if (P.omega) {

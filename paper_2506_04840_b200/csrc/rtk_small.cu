@@ -741,7 +741,15 @@ __global__ void __launch_bounds__(256) final_u_kernel(const double* __restrict__
     }
     __syncthreads();
   }
-  const double sg = col[si[0]] < 0.0 ? -1.0 : 1.0;
+  // ties: |entries| within 1e-5 of the maximum count as tied, lowest row wins (reading C6)
+  const double thr = (1.0 - 1e-5) * sb[0];
+  __shared__ int piv;
+  if (threadIdx.x == 0) piv = 0x7fffffff;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (fabs(col[i]) >= thr) { atomicMin(&piv, i); break; }
+  __syncthreads();
+  const double sg = col[piv == 0x7fffffff ? 0 : piv] < 0.0 ? -1.0 : 1.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) U[(int64_t)c * n + i] = (float)(sg * col[i]);
 }
 

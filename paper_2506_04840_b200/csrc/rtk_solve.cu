@@ -47,6 +47,7 @@ constexpr int kST = 256;       // threads per CTA
 constexpr int kRBr = 8;        // rows per reduce_gram CTA
 constexpr int kChunk = 64;     // rows per product chunk in step_kernel
 constexpr int kMaxC = 8;       // cluster size (portable maximum)
+constexpr double kPinTie = 1e-5;   // sign pin: |entries| within this (relative) of the max are tied (C6)
 
 __device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
   int t = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
@@ -1121,14 +1122,24 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       }
     }
     cluster.sync();
+    // ties: |entries| within kPinTie of the column maximum count as tied (reading C6): the pivot is
+    // the lowest such row over the cluster (second reduction, indices in amax + kMaxC * 2 * kSL)
+    double* amax2 = a.amax + (int64_t)kMaxC * 2 * kSL;
     for (int c = warp; c < a.r; c += kST / 32) {
       double best = -1.0;
+      for (int b = 0; b < C; ++b) best = fmax(best, ldcg(a.amax + (int64_t)b * 2 * kSL + 2 * c));
+      const double thr = (1.0 - kPinTie) * best;
       int bi = 0x7fffffff;
-      for (int b = 0; b < C; ++b) {
-        const double v = ldcg(a.amax + (int64_t)b * 2 * kSL + 2 * c);
-        const int iv = (int)ldcg(a.amax + (int64_t)b * 2 * kSL + 2 * c + 1);
-        if (v > best || (v == best && iv < bi)) { best = v; bi = iv; }
-      }
+      for (int i = r0 + lane; i < r1; i += 32)
+        if (fabs(a.Qd[(int64_t)c * n + i]) >= thr) { bi = i; break; }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) bi = min(bi, __shfl_xor_sync(0xffffffffu, bi, o));
+      if (lane == 0) amax2[(int64_t)rank * kSL + c] = (double)bi;
+    }
+    cluster.sync();
+    for (int c = warp; c < a.r; c += kST / 32) {
+      int bi = 0x7fffffff;
+      for (int b = 0; b < C; ++b) bi = min(bi, (int)ldcg(amax2 + (int64_t)b * kSL + c));
       const double sgn = ldcg(a.Qd + (int64_t)c * n + bi) < 0.0 ? -1.0 : 1.0;
       if (lane == 0) S.colscale[c] = sgn;
       for (int i = r0 + lane; i < r1; i += 32) a.U[(int64_t)c * n + i] = (float)(sgn * a.Qd[(int64_t)c * n + i]);
@@ -1337,13 +1348,26 @@ __global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q,
   }
   if ((tid & 31) == 0) { bv[tid >> 5] = (bval < 0.0) ? -best : best; bi[tid >> 5] = bidx; }
   __syncthreads();
-  __shared__ double sgn_s;
+  __shared__ double sgn_s, thr_s;
+  __shared__ int piv_s;
   if (tid == 0) {
-    double b = -1.0, v = 0.0;
-    int ix = 0x7fffffff;
-    for (int w = 0; w < kST / 32; ++w)
-      if (fabs(bv[w]) > b || (fabs(bv[w]) == b && bi[w] < ix)) { b = fabs(bv[w]); ix = bi[w]; v = bv[w]; }
-    sgn_s = v < 0.0 ? -1.0 : 1.0;
+    double b = -1.0;
+    for (int w = 0; w < kST / 32; ++w) b = fmax(b, fabs(bv[w]));
+    thr_s = (1.0 - kPinTie) * b;   // ties within kPinTie of the maximum (reading C6)
+    piv_s = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kST) {   // lowest row whose |u_i| reaches the tie threshold
+    double u = 0.0;
+    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+    if (fabs(u) >= thr_s) { atomicMin(&piv_s, i); break; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double u = 0.0;
+    const int i = piv_s == 0x7fffffff ? 0 : piv_s;
+    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+    sgn_s = u < 0.0 ? -1.0 : 1.0;
   }
   __syncthreads();
   const double sgn = sgn_s;

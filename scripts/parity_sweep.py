@@ -92,7 +92,13 @@ def main():
         gU = [u.cpu().numpy() for u in g_U]
         re_g = metrics.relative_error(a, g_core.cpu().numpy(), gU)
         re_o = metrics.relative_error(a, orc.core, orc.factors)
-        gaps = metrics.mode_gaps(a, ranks, orc.factors, seq)
+        gaps = list(metrics.mode_gaps(a, ranks, orc.factors, seq))
+        if c["algo"] == "a2":   # U_k is unique only up to the l-core unfolding's column count
+            ls = [r + c["p"] for r in ranks]
+            for k in range(len(dims)):
+                cols = int(np.prod(ranks[:k]) * np.prod(ls[k + 1:]))
+                if ranks[k] > cols:
+                    gaps[k] = 0.0   # null-space completion: any orthonormal choice is valid
         orth = max(metrics.orthonormality(u) for u in gU)
         ang = max([metrics.max_principal_angle(uo, ug) for uo, ug, gp in zip(orc.factors, gU, gaps) if gp > 0.1]
                   or [0.0])

@@ -231,7 +231,11 @@ def _a2_check(a, ranks, p, q, seed, shift=True, alpha_rtol=1e-3):
     assert abs(re_g - re_o) <= RE_TOL * re_o + 1e-7, (re_g, re_o)
     for u in g_U:
         assert metrics.orthonormality(u) <= ORTH_TOL
-    gaps = metrics.mode_gaps(a, ranks, orc.factors, True)
+    gaps = list(metrics.mode_gaps(a, ranks, orc.factors, True))
+    ls = [r + p for r in ranks]
+    for k in range(len(ranks)):   # r_k beyond the l-core unfolding's columns: null-space completion
+        if ranks[k] > int(np.prod(ranks[:k]) * np.prod(ls[k + 1:])):
+            gaps[k] = 0.0
     for k, u in enumerate(g_U):
         if gaps[k] > 0.10:
             assert metrics.max_principal_angle(orc.factors[k], u) <= ANGLE_TOL, (k, gaps[k])
