@@ -165,6 +165,8 @@ struct Layout {
   size_t g2part = 0, gsum = 0, amax = 0;
   size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
   size_t om = 0, omtab = 0;                                         // Appendix D sketches only
+  size_t mode_size = 0;   // bytes of one mode's scratch region (T-HOSVD: one region per mode)
+  int nregions = 1;
   size_t shr_elems = 0;
   std::vector<TilePlan> sk, pw, sh;
 };
@@ -223,6 +225,26 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off += align_up(std::max<size_t>(bytes, 16)); return o; };
   L.ldw = ldw;
+  // global region: per-mode report slots, the shrink chain buffers, Alg. A.2's l-core stage
+  L.alpha = take(P.d * 8);
+  L.trace = take((size_t)P.d * P.q * 8);
+  L.sigma = take((size_t)P.d * 128 * 8);
+  L.status = take((size_t)P.d * 4 * 4);
+  L.shr0 = take(shr * 4);
+  L.shr1 = take(shr * 4);
+  if (P.a2) {
+    size_t qa = 0, lt = 1;
+    for (int k = 0; k < P.d; ++k) { qa += (size_t)P.dims[k] * P.keep[k]; lt *= (size_t)P.keep[k]; }
+    L.a2q = take(qa * 8);
+    L.a2b = take(lt * 4);
+    L.a2g0 = take(lt * 8);
+    L.a2g1 = take(lt * 8);
+    L.a2gram = take((size_t)kSolveLMax * kSolveLMax * 8);
+    L.a2v = take((size_t)kSolveLMax * kSolveLMax * 8);
+  }
+  // mode region (offsets of region 0; T-HOSVD gives every mode its own copy so that the modes,
+  // which are independent in Alg. 3, run concurrently on their own streams)
+  const size_t mode0 = off;
   L.planes = take(planes * 4);
   L.wbuf = take(wbuf * 4);
   L.ypart = take(ypart * 4);
@@ -233,16 +255,10 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.gpart = take(gp * 8);
   L.T = take(ll * 8);
   L.lam = take(lmax * 8);
-  L.alpha = take(P.d * 8);
-  L.trace = take((size_t)P.d * P.q * 8);
-  L.sigma = take((size_t)P.d * 128 * 8);
-  L.status = take((size_t)P.d * 4 * 4);
   L.sighat = take(lmax * 8);
   L.g2part = take((size_t)8 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.amax = take((size_t)8 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices
-  L.shr0 = take(shr * 4);
-  L.shr1 = take(shr * 4);
   if (P.omega) {
     size_t oms = 0, tabs = 0;
     for (int k = 0; k < P.d; ++k) {
@@ -254,16 +270,9 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
     L.om = take(oms * 4);
     L.omtab = take(tabs * 4);
   }
-  if (P.a2) {
-    size_t qa = 0, lt = 1;
-    for (int k = 0; k < P.d; ++k) { qa += (size_t)P.dims[k] * P.keep[k]; lt *= (size_t)P.keep[k]; }
-    L.a2q = take(qa * 8);
-    L.a2b = take(lt * 4);
-    L.a2g0 = take(lt * 8);
-    L.a2g1 = take(lt * 8);
-    L.a2gram = take((size_t)kSolveLMax * kSolveLMax * 8);
-    L.a2v = take((size_t)kSolveLMax * kSolveLMax * 8);
-  }
+  L.mode_size = off - mode0;
+  L.nregions = P.seq ? 1 : P.d;
+  off += (size_t)(L.nregions - 1) * L.mode_size;
   L.total = off;
   return L;
 }
@@ -274,15 +283,15 @@ struct Side {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_step = nullptr, ev_alpha = nullptr;
 };
-cudaError_t side_streams(Side** out) {
+cudaError_t side_streams(Side** out, int idx = 0) {   // idx: one set per concurrently running mode
   static std::mutex mu;
-  static Side S[64];
+  static Side S[64][8];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (dev < 0 || dev >= 64 || idx < 0 || idx >= 8) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(mu);
-  Side& s = S[dev];
+  Side& s = S[dev][idx];
   if (!s.aux) {
     e = cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming);
@@ -290,6 +299,32 @@ cudaError_t side_streams(Side** out) {
     if (e != cudaSuccess) return e;
   }
   *out = &s;
+  return cudaSuccess;
+}
+
+// Per-device streams + fork/join events for Alg. 3's concurrent modes.
+struct ModeStreams {
+  cudaStream_t s[8] = {};
+  cudaEvent_t fork = nullptr, join[8] = {};
+};
+cudaError_t mode_streams(ModeStreams** out) {
+  static std::mutex mu;
+  static ModeStreams M[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  ModeStreams& m = M[dev];
+  if (!m.fork) {
+    for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
+      e = cudaStreamCreateWithFlags(&m.s[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m.join[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m.fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *out = &m;
   return cudaSuccess;
 }
 
@@ -303,25 +338,26 @@ cudaError_t side_streams(Side** out) {
 int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, uint64_t seed,
              bool shift, float* Uk, cudaStream_t st) {
   const int n = v.n, r = P.ranks[k], l = r + P.p;
+  char* mw = ws + (P.seq ? 0 : (size_t)k * L.mode_size);   // this mode's scratch region
   ModeBufs B;
   B.n = n; B.l = l; B.r = P.a2 ? l : r;   // A.2: the step kernel pins all l columns of Q
-  B.Ypart = (float*)(ws + L.ypart);
-  B.Y = (double*)(ws + L.y);
-  B.Q1 = (double*)(ws + L.q1);
-  B.Qd = (double*)(ws + L.qd);
-  B.Qs = (float*)(ws + L.qs);
-  B.gpart = (double*)(ws + L.gpart);
+  B.Ypart = (float*)(mw + L.ypart);
+  B.Y = (double*)(mw + L.y);
+  B.Q1 = (double*)(mw + L.q1);
+  B.Qd = (double*)(mw + L.qd);
+  B.Qs = (float*)(mw + L.qs);
+  B.gpart = (double*)(mw + L.gpart);
   B.nblk = (n + 63) / 64;   // kGB-row Gram blocks (rtk_small.cu)
-  B.T = (double*)(ws + L.T);
-  B.lam = (double*)(ws + L.lam);
+  B.T = (double*)(mw + L.T);
+  B.lam = (double*)(mw + L.lam);
   B.alpha = (double*)(ws + L.alpha) + k;
   B.trace = (double*)(ws + L.trace) + (size_t)k * P.q;
   B.sigma = (double*)(ws + L.sigma) + (size_t)k * 128;
   B.status = (int*)(ws + L.status) + 4 * k;
-  B.sighat = (double*)(ws + L.sighat);
-  B.g2part = (double*)(ws + L.g2part);
-  B.gsum = (double*)(ws + L.gsum);
-  B.amax = (double*)(ws + L.amax);
+  B.sighat = (double*)(mw + L.sighat);
+  B.g2part = (double*)(mw + L.g2part);
+  B.gsum = (double*)(mw + L.gsum);
+  B.amax = (double*)(mw + L.amax);
   const bool fast = l <= kSolveLMax;   // cluster small solver (rtk_solve.cu)
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
   const uint32_t mode1 = (uint32_t)(k + 1);
@@ -333,23 +369,23 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   const int* stop = pve ? B.status + 3 : nullptr;
   if (pve) RTK_CK(cudaMemsetAsync(B.sighat, 0, (size_t)l * sizeof(double), st));   // sigmahat = 0
   const bool defer = fast && tc && P.q > 1 && !pve;   // deferred shift updates on the side stream
-  if (defer) RTK_CK(side_streams(&side));
+  if (defer) RTK_CK(side_streams(&side, k));
   bool pending = false;                       // an alpha_kernel is in flight on side->aux
   const float* om = nullptr;   // Appendix D sketch types: Omega_k materialised once per mode
   if (P.omega) {
     const std::vector<int64_t> e = cur_dims(P, k);
     ProfScope ps(0, k, st);
-    om = (const float*)(ws + L.om);
-    RTK_CK(sketch_materialize(P.omega, seed, k + 1, e.data(), P.d, 0, v.m(), l, (float*)(ws + L.omtab),
-                              (float*)(ws + L.om), st));
+    om = (const float*)(mw + L.om);
+    RTK_CK(sketch_materialize(P.omega, seed, k + 1, e.data(), P.d, 0, v.m(), l, (float*)(mw + L.omtab),
+                              (float*)(mw + L.om), st));
     g_launches += 1 + (P.omega >= 2 ? P.d - 1 : 0);
   }
   for (int step = 0; step <= P.q; ++step) {
     const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
     if (tc) {
       ProfScope ps(step == 0 ? 0 : 1, k, st);
-      float* planes = (float*)(ws + L.planes);
-      float* W = (float*)(ws + L.wbuf);
+      float* planes = (float*)(mw + L.planes);
+      float* W = (float*)(mw + L.wbuf);
       const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
       // sketch on the fused engine only for long unfoldings (Omega-plane generation has a fixed
       // cost; tc_op2 generates Omega in shared memory and is faster for small m)
@@ -395,7 +431,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     }
     if (fast) {
       ProfScope ps(3, k, st);
-      float* planes = tc ? (float*)(ws + L.planes) : nullptr;
+      float* planes = tc ? (float*)(mw + L.planes) : nullptr;
       if (pending) {   // the previous step's alpha is needed by this reduce (Y = M M^T Q - alpha Q)
         RTK_CK(cudaStreamWaitEvent(st, side->ev_alpha, 0));
         pending = false;
@@ -412,7 +448,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       }
       // B.1 may stop at any power step: U_k is written by the step that stops (or the last)
       // A.2: the pinned fp32 basis replaces the shadow Qs (the shrink's matrix), Qd pinned in place
-      float* uout = P.a2 ? (float*)(ws + L.qs) : Uk;
+      float* uout = P.a2 ? (float*)(mw + L.qs) : Uk;
       RTK_CK(launch_step(B, step, P.q, shift, (step == P.q || (pve && step > 0)) ? uout : nullptr, seed, mode1,
                          planes, tc_npad(l), (int)pad4(n), dstep, pve ? P.pve : 0.0, st, P.a2));
       g_launches += 2;
@@ -557,12 +593,19 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
       if (rc) return rc;
     }
   } else {
-    // Alg. 3: every mode factors the original A_(k) through its strided view
+    // Alg. 3: every mode factors the original A_(k) through its strided view; the modes are
+    // independent, so each runs on its own stream in its own scratch region (fork / join events)
+    ModeStreams* ms = nullptr;
+    RTK_CK(mode_streams(&ms));
+    RTK_CK(cudaEventRecord(ms->fork, st));
     for (int k = 0; k < d; ++k) {
+      RTK_CK(cudaStreamWaitEvent(ms->s[k], ms->fork, 0));
       const View rv = range_view(P, k, A, nullptr);
-      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], ms->s[k]);
       if (rc) return rc;
+      RTK_CK(cudaEventRecord(ms->join[k], ms->s[k]));
     }
+    for (int k = 0; k < d; ++k) RTK_CK(cudaStreamWaitEvent(st, ms->join[k], 0));
     // core = A x_1 U_1^T ... x_d U_d^T, same shrink chain
     for (int k = 0; k < d; ++k) {
       const float* cur = k == 0 ? A : shr[(k - 1) & 1];
