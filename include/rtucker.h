@@ -21,7 +21,11 @@
  *
  * OWNERSHIP.  The caller allocates and owns A, every U[k], core and ws; the
  * library never frees them and never writes A.  The library keeps no state
- * between calls except a per-thread error string and cached kernel attributes.
+ * between calls except a per-thread error string, cached kernel attributes and,
+ * per host thread and device, a small pool of internal streams and events (the
+ * side stream of the deferred shift update and Alg. 3's per-mode streams, joined
+ * back into `stream` before the call returns its work).  A ws shared by two
+ * calls must not be in use by both at once (ordinary stream ordering suffices).
  * If ws == NULL the call allocates (cudaMallocAsync) and frees its own
  * workspace on the stream.
  *

@@ -283,14 +283,14 @@ struct Side {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_step = nullptr, ev_alpha = nullptr;
 };
+// The pools are per host thread (thread_local): concurrent rtk_solve calls from different host
+// threads never share fork/join events or side streams.
 cudaError_t side_streams(Side** out, int idx = 0) {   // idx: one set per concurrently running mode
-  static std::mutex mu;
-  static Side S[64][8];
+  static thread_local Side S[64][8];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64 || idx < 0 || idx >= 8) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lk(mu);
   Side& s = S[dev][idx];
   if (!s.aux) {
     e = cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking);
@@ -308,13 +308,11 @@ struct ModeStreams {
   cudaEvent_t fork = nullptr, join[8] = {};
 };
 cudaError_t mode_streams(ModeStreams** out) {
-  static std::mutex mu;
-  static ModeStreams M[64];
+  static thread_local ModeStreams M[64];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lk(mu);
   ModeStreams& m = M[dev];
   if (!m.fork) {
     for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
