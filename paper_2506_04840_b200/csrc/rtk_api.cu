@@ -302,6 +302,27 @@ cudaError_t side_streams(Side** out, int idx = 0) {   // idx: one set per concur
   return cudaSuccess;
 }
 
+// plan() is pure host work (tile-plan search per mode); repeated solves of one shape reuse it.
+// The key holds every input plan() reads, including its environment overrides.
+const Layout& plan_cached(const Problem& P, int nsm, const float* A, int path) {
+  static thread_local std::vector<std::pair<std::string, Layout>> cache;
+  std::string key;
+  auto add = [&](long long x) { key += std::to_string(x); key += ','; };
+  add(P.d); add(P.p); add(P.q); add(P.seq); add(P.a2); add(P.omega); add(nsm); add(path);
+  add((long long)((uintptr_t)A % 16));
+  for (int k = 0; k < P.d; ++k) { add(P.dims[k]); add(P.ranks[k]); add(P.keep[k]); }
+  for (const char* ev : {"RTK_PATH", "RTK_PLAN", "RTK_PLAN_SKETCH", "RTK_PLAN_POWER", "RTK_PLAN_SHRINK"}) {
+    const char* v = getenv(ev);
+    key += v ? v : "-";
+    key += ';';
+  }
+  for (auto& kv : cache)
+    if (kv.first == key) return kv.second;
+  if (cache.size() >= 16) cache.erase(cache.begin());
+  cache.emplace_back(key, plan(P, nsm, A, path));
+  return cache.back().second;
+}
+
 // Per-device streams + fork/join events for Alg. 3's concurrent modes.
 struct ModeStreams {
   cudaStream_t s[8] = {};
@@ -539,7 +560,7 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (opt.path < 0 || opt.path > 2) return fail(RTK_ERR_ARG, "path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
-  const Layout L = plan(P, num_sms(), A, opt.path);
+  const Layout L = plan_cached(P, num_sms(), A, opt.path);
   if (opt.path == 2)
     for (int k = 0; k < d; ++k)
       if (!L.tc_range[k]) return fail(RTK_ERR_SHAPE, "tcgen05 path unavailable for mode " + std::to_string(k + 1));
@@ -716,7 +737,7 @@ size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32
   P.ranks.assign(ranks, ranks + d);
   set_keep(P);
   if (validate(P)) return 0;
-  return plan(P, num_sms(), nullptr, o.path).total;
+  return plan_cached(P, num_sms(), nullptr, o.path).total;
 }
 
 int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out, void* stream) {
