@@ -383,3 +383,55 @@ def test_a2_rank_exceeds_core_rank():
     re_g = metrics.relative_error(a, core.cpu().numpy(), gU)
     re_o = metrics.relative_error(a, orc.core, orc.factors)
     assert abs(re_g - re_o) <= RE_TOL * re_o
+
+
+# ------------------------------------------------------------ C5 at full size (the bench's launch)
+def test_c5_full_size_properties():
+    """BASELINE C5 (1000^3, r = 50, p = 10, q = 5) through the public API exactly as bench.py runs
+    it, checked where the float64 oracle cannot follow at this size: sampled core entries recomputed
+    one by one in fp64 from the factors, the core identity ||A||^2 - ||core||^2 = ||A - A_hat||^2,
+    orthonormal factors, alpha monotone and below lambda_l(A_(1) A_(1)^T)/2, and
+    mode 1's projection error within 1 % of the optimum from the exact Gram eigenvalues."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import rsthosvd
+    from workloads import make_config_tensor_torch
+    c = CONFIGS["c5"]
+    A = make_config_tensor_torch("c5")                      # (1000, 1000, 1000) column-major fp32
+    core, U, rep = rsthosvd(A, c["ranks"], c["p"], c["q"], c["omega_seed"], report=True)
+    torch.cuda.synchronize()
+    assert rep.numeric == 0
+    Ud = [u.double() for u in U]
+    for u in Ud:
+        assert torch.linalg.matrix_norm(u.T @ u - torch.eye(u.shape[1], device=u.device, dtype=torch.float64)) <= ORTH_TOL
+    # A_(1)^T as a (n2 n3) x n1 view (rows of the C-contiguous (n3, n2, n1) tensor)
+    X = A.permute(2, 1, 0).reshape(-1, A.shape[0])
+    n1 = A.shape[0]
+    G = torch.zeros((n1, n1), dtype=torch.float64, device=A.device)
+    for s0 in range(0, X.shape[0], 100000):
+        xc = X[s0:s0 + 100000].double()
+        G += xc.T @ xc
+    lam = torch.linalg.eigvalsh(G).flip(0)                 # descending
+    l = c["ranks"][0] + c["p"]
+    al = [0.0] + list(rep.alpha_trace[0])
+    assert all(b >= a0 for a0, b in zip(al, al[1:]))
+    assert max(rep.alpha_trace[0]) <= lam[l - 1].item() / 2 * (1 + 1e-6)
+    r1 = c["ranks"][0]
+    opt = lam[r1:].sum().item()
+    proj = (torch.trace(G) - torch.trace(Ud[0].T @ G @ Ud[0])).item()
+    assert opt <= proj <= 1.01 * opt, (proj, opt)
+    # sampled core entries, one by one: core[a,b,c] = sum A[i,j,k] U1[i,a] U2[j,b] U3[k,c]
+    g = torch.Generator(device="cpu").manual_seed(3)
+    idx = [tuple(int(torch.randint(0, r, (1,), generator=g)) for r in c["ranks"]) for _ in range(6)]
+    for (a_, b_, c_) in idx:
+        t = torch.zeros((), dtype=torch.float64, device=A.device)
+        for k0 in range(0, A.shape[2], 100):
+            slab = A[:, :, k0:k0 + 100].double()
+            t += torch.einsum("ijk,i,j,k->", slab, Ud[0][:, a_], Ud[1][:, b_], Ud[2][k0:k0 + 100, c_])
+        ref = t.item()
+        got = core[a_, b_, c_].item()
+        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)) + 1e-6 * core.abs().max().item(), ((a_, b_, c_), got, ref)
+    # core identity for orthonormal factors: ||A - A_hat||^2 = ||A||^2 - ||core||^2
+    a2 = sum((A[:, :, k0:k0 + 100].double() ** 2).sum().item() for k0 in range(0, A.shape[2], 100))
+    c2 = (core.double() ** 2).sum().item()
+    re = ((a2 - c2) / a2) ** 0.5
+    assert 0.94 < re < 0.97, re                              # SURVEY 8(d): RE ~ 0.955 for this recipe
