@@ -334,11 +334,20 @@ __device__ void tri_inv_upper(const double* R, double* T, int l, double* /*unuse
 // Thread (i = tid/4, part = tid%4) keeps A(i, part + 4jj), jj < 16, in registers.  The quad that
 // owns row k builds reflector k from its registers (quad shuffles only): v_k on rows k+1..l-1
 // with v_k(k+1) = x0 - alpha is stored in Hv row k, beta_k in hb[k].  Two barriers per reflector.
-__device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
-                        double* pvbuf, double* scal) {
+// ACC: also accumulate QH = H_0 H_1 ... H_{l-3} (thread (i, part) keeps row i's columns part + 4jj in
+// registers, the same layout as A) and write it to QH (ld kLD) at the end: the eigenvectors of A are
+// then QH Z for those Z of the tridiagonal, one dense product instead of l - 2 reflector sweeps.
+template <bool ACC>
+__device__ void tridiag_t(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
+                          double* pvbuf, double* scal, double* QH) {
   const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
   const unsigned qm = 0xFu << ((tid & 31) & ~3);
   double w[16];
+  double qh[ACC ? 16 : 1];
+  if (ACC) {
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) qh[jj] = (i < l && part + 4 * jj == i) ? 1.0 : 0.0;
+  }
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) {
     const int j = part + 4 * jj;
@@ -401,6 +410,16 @@ __device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* 
       double s = (s0 + s1) + (s2 + s3);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
+      double uq = 0.0;   // (QH v)_i
+      if (ACC) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = part + 4 * jj;
+          if (j > k && j < l) uq = fma(qh[jj], v[j], uq);
+        }
+        uq += __shfl_xor_sync(0xffffffffu, uq, 1);
+        uq += __shfl_xor_sync(0xffffffffu, uq, 2);
+      }
       if (part == 0) {
         const bool act = i > k && i < l;
         pbuf[i] = act ? beta * s : 0.0;
@@ -414,6 +433,14 @@ __device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* 
 #pragma unroll
       for (int o = 16; o; o >>= 1) t0 += __shfl_xor_sync(0xffffffffu, t0, o);
       const double K = 0.5 * beta * t0;
+      if (ACC && i < l) {   // QH <- QH - beta (QH v) v^T on columns k+1..l-1
+        const double bu = beta * uq;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = part + 4 * jj;
+          if (j > k && j < l) qh[jj] = fma(-bu, v[j], qh[jj]);
+        }
+      }
       if (i > k && i < l) {
         const double vi = v[i], wi = pbuf[i] - K * vi;
 #pragma unroll
@@ -445,6 +472,37 @@ __device__ void tridiag(const double* A, int l, double* Hv, double* hb, double* 
     }
   } else if (i == 0 && part == 0) {
     d[0] = w[0];
+  }
+  if (ACC && i < l) {
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = part + 4 * jj;
+      if (j < l) QH[i * kLD + j] = qh[jj];
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void tridiag(const double* A, int l, double* Hv, double* hb, double* d, double* e,
+                                        double* pbuf, double* pvbuf, double* scal) {
+  tridiag_t<false>(A, l, Hv, hb, d, e, pbuf, pvbuf, scal, nullptr);
+}
+
+// Out(i, c) = sum_j QH(i, j) Z(j, c), i, c < l (all ld kLD): thread (i, part) computes columns
+// part + 4cc of row i.
+__device__ void qh_times_z(const double* QH, const double* Z, int l, double* Out) {
+  const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
+  if (i < l) {
+    double acc[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
+    for (int j = 0; j < l; ++j) {
+      const double q = QH[i * kLD + j];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(q, Z[j * kLD + part + 4 * cc], acc[cc]);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc)
+      if (part + 4 * cc < l) Out[i * kLD + part + 4 * cc] = acc[cc];
   }
   __syncthreads();
 }
@@ -899,18 +957,24 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   }
   if (eig) {
     tck[ntck++] = clock64();
-    if (!have_eigs) {   // tridiag / all_eigs results are still intact when B.1 computed them
-      tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+    double* Z = S.G;    // G no longer needed
+    if (!have_eigs) {
+      // tridiagonalise with the accumulated reflector product QH (into T: free until the rows)
+      tridiag_t<true>(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal, S.T);
       for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
       __syncthreads();
       tck[ntck++] = clock64();
       all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+      tck[ntck++] = clock64();
+      tri_eigvecs(S.d, S.e, S.lam, l, S.H, S.R);   // tridiagonal's eigenvectors (Householder rows done)
+      tck[ntck++] = clock64();
+      qh_times_z(S.T, S.H, l, Z);                  // A's eigenvectors = QH Z
+    } else {            // tridiag / all_eigs results are still intact when B.1 computed them
+      tck[ntck++] = clock64();
+      tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R);
+      tck[ntck++] = clock64();
+      back_transform(S.H, S.hb, l, Z);
     }
-    tck[ntck++] = clock64();
-    double* Z = S.G;    // G no longer needed
-    tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R);
-    tck[ntck++] = clock64();
-    back_transform(S.H, S.hb, l, Z);
     // T(:, cc) = V(:, l-1-cc) / sqrt(lambda): descending order; null columns flagged
     const double sg1 = sqrt(fmax(S.lam[l - 1], 0.0));
     if (tid == 0) S.flags[1] = 0;
@@ -1268,13 +1332,13 @@ __global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int idx = tid; idx < c * c; idx += kST) S.G[(idx / c) * kLD + idx % c] = gram[idx];
   __syncthreads();
-  tridiag(S.G, c, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
+  tridiag_t<true>(S.G, c, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal, S.R);   // QH -> R
   for (int k = tid; k + 1 < c; k += kST) S.e2[k] = S.e[k] * S.e[k];
   __syncthreads();
   all_eigs(S.d, S.e, S.e2, c, S.lam, S.blo, S.bhi, S.cnt);
   double* Z = S.G;
-  tri_eigvecs(S.d, S.e, S.lam, c, Z, S.R);
-  back_transform(S.H, S.hb, c, Z);
+  tri_eigvecs(S.d, S.e, S.lam, c, S.H, S.G);   // tridiagonal's eigenvectors into H (G is scratch)
+  qh_times_z(S.R, S.H, c, Z);                  // eigenvectors of the Gram = QH Z
   // descending order into R: R(i, cc) = Z(i, c-1-cc)
   for (int idx = tid; idx < c * r; idx += kST) {
     const int i = idx % c, cc = idx / c;
