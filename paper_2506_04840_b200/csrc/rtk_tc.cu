@@ -317,17 +317,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
         const int sb = (int)(ib % SB);
         bar_wait(&emptyB[sb], (uint32_t)(((ib / SB) & 1) ^ 1));
         uint8_t* bt = smB + sb * STB;
-        for (int it2 = tid; it2 < kBK * (N / 2); it2 += 128) {
-          const int jj = it2 % kBK, c2 = (it2 / kBK) * 2;
+        for (int it2 = tid; it2 < kBK * (N / 4); it2 += 128) {   // one Philox block per 4 columns
+          const int jj = it2 % kBK, c4 = (it2 / kBK) * 4;
           const int64_t j = kc * kBK + jj;
-          float2 z = make_float2(0.f, 0.f);
-          if (j < a.m && c2 < a.l) z = sketch_pair(a.om, a.l, a.seed, a.mode, (uint64_t)j, c2);
-          const float z1 = (c2 + 1 < a.l) ? z.y : 0.f;
-          const float h0 = tf32_rna(z.x), h1 = tf32_rna(z1);
-          *reinterpret_cast<float*>(bt + sw128_offset(c2, jj)) = h0;
-          *reinterpret_cast<float*>(bt + BB + sw128_offset(c2, jj)) = z.x - h0;
-          *reinterpret_cast<float*>(bt + sw128_offset(c2 + 1, jj)) = h1;
-          *reinterpret_cast<float*>(bt + BB + sw128_offset(c2 + 1, jj)) = z1 - h1;
+          float z[4] = {0.f, 0.f, 0.f, 0.f};
+          if (j < a.m && c4 < a.l) {
+            if (a.om) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (c4 + u < a.l) z[u] = a.om[(uint64_t)j * a.l + c4 + u];
+            } else {
+              const uint4 x = omega_bits(a.seed, a.mode, (uint64_t)j, (uint32_t)(c4 >> 2));
+              const float2 z01 = box_muller(x.x, x.y);
+              z[0] = z01.x; z[1] = c4 + 1 < a.l ? z01.y : 0.f;
+              if (c4 + 2 < a.l) {
+                const float2 z23 = box_muller(x.z, x.w);
+                z[2] = z23.x; z[3] = c4 + 3 < a.l ? z23.y : 0.f;
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float h = tf32_rna(z[u]);
+            *reinterpret_cast<float*>(bt + sw128_offset(c4 + u, jj)) = h;
+            *reinterpret_cast<float*>(bt + BB + sw128_offset(c4 + u, jj)) = z[u] - h;
+          }
         }
         fence_async_smem();
         __syncwarp();
