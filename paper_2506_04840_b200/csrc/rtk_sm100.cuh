@@ -105,6 +105,16 @@ __device__ __forceinline__ void umma_commit(uint64_t* b) {
                : "memory");
 }
 // 32 lanes x 32b, 16 consecutive columns per thread
+// 16 lanes x 32 consecutive 32-bit columns (shape 16x256b repeated 4 times along the columns):
+// thread T holds, for repeat r, lane T/4 columns 8r + 2(T%4) + {0,1} in v[4r], v[4r+1] and lane
+// T/4 + 8, same columns, in v[4r+2], v[4r+3] (scripts/micro/tmem_shape.cu checks this layout)
+__device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
