@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op1_kernel(const __grid_cons
   constexpr int TCOLS = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : 128;
   constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
   extern __shared__ __align__(1024) uint8_t smraw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  // 1024-B aligned base, derived by an offset from smraw so that the compiler keeps the shared
+  // address space (LDS / STS instead of generic LD.E / ST.E through the smem window)
+  uint8_t* sm = smraw + ((1024u - (smem_addr(smraw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full[S], lofull[S], empty[S], accf[2], acce[2];
   __shared__ uint32_t tbase_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -215,7 +217,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
   constexpr int STB = 2 * BB;                   // B hi + lo
   constexpr uint32_t IDESC = idesc_tf32(128, N, 1, 0);   // A MN-major, B K-major
   extern __shared__ __align__(1024) uint8_t smraw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  // 1024-B aligned base, derived by an offset from smraw so that the compiler keeps the shared
+  // address space (LDS / STS instead of generic LD.E / ST.E through the smem window)
+  uint8_t* sm = smraw + ((1024u - (smem_addr(smraw) & 1023u)) & 1023u);
   uint8_t* smA = sm;
   uint8_t* smB = sm + SA * STA;
   __shared__ __align__(8) uint64_t fullA[SA], loA[SA], emptyA[SA], fullB[SB], emptyB[SB], accf;
