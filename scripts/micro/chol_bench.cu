@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(256, 1) bench(const double* Gg, int l, long lo
   long long t0 = clock64();
   bool ok = chol_upper(S.G, S.R, S.rowbuf, l);
   long long t1 = clock64();
-  tri_inv_upper(S.R, S.T, l, S.lam);
+  tri_inv_upper(S.R, S.T, l, S.rowbuf);
   long long t2 = clock64();
   tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
   long long t3 = clock64();
