@@ -256,9 +256,9 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.T = take(ll * 8);
   L.lam = take(lmax * 8);
   L.sighat = take(lmax * 8);
-  L.g2part = take((size_t)8 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);
+  L.g2part = take((size_t)16 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);   // <= 16 cluster CTAs
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
-  L.amax = take((size_t)8 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices
+  L.amax = take((size_t)16 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 16 CTAs
   if (P.omega) {
     size_t oms = 0, tabs = 0;
     for (int k = 0; k < P.d; ++k) {

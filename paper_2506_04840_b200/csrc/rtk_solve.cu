@@ -46,7 +46,7 @@ constexpr int kMLD = 66;       // leading dimension of T (even: 16-byte double2 
 constexpr int kST = 256;       // threads per CTA
 constexpr int kRBr = 8;        // rows per reduce_gram CTA
 constexpr int kChunk = 64;     // rows per product chunk in step_kernel
-constexpr int kMaxC = 8;       // cluster size (portable maximum)
+constexpr int kMaxC = 16;      // cluster size (16: non-portable opt-in, checked by occupancy query)
 constexpr double kPinTie = 1e-5;   // sign pin: |entries| within this (relative) of the max are tied (C6)
 
 __device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
@@ -1502,8 +1502,44 @@ cudaError_t a2_finish(const float* B, int d, const int* l, const int* r, const i
 // ---------------------------------------------------------------- host side
 double* g_step_dbg = nullptr;   // diagnostics: set by rtk_debug_clocks (not part of the product path)
 
+// one 64-row chunk per CTA where the cluster can hold it: up to 8 CTAs (portable) or 16 when the
+// device schedules a 16-CTA cluster of step_kernel (non-portable size; queried once per device).
+// RTK_STEP_CLUSTER=8 caps it (A/B timing).
+static int max_step_cluster() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 8;
+  if (cached[dev]) return cached[dev];
+  int best = 8;
+  const char* ev = getenv("RTK_STEP_CLUSTER");
+  const int cap = ev ? atoi(ev) : 16;
+  if (cap >= 16 &&
+      cudaFuncSetAttribute(step_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+      cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StepSmem)) ==
+          cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(kST, 1, 1);
+    cfg.dynamicSmemBytes = sizeof(StepSmem);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, step_kernel, &cfg) == cudaSuccess && nc >= 1) best = 16;
+  }
+  cudaGetLastError();   // a refused query leaves no sticky error
+  cached[dev] = best;
+  return best;
+}
+
 int solve_cluster_size(int n) {
-  int C = (n + 127) / 128;
+  int C = (n + kChunk - 1) / kChunk;
+  if (C > 8) C = std::min(C, max_step_cluster());
   return std::max(1, std::min(kMaxC, C));
 }
 
