@@ -93,6 +93,7 @@ cudaError_t launch_sum_partials(const float* Ypart, int G, int ltot, int n_rows,
                                 double* Y, cudaStream_t st);
 
 int num_sms();
+bool pdl_enabled();   // programmatic dependent launch for the per-step kernels (RTK_PDL=0: off)
 
 // ---- cluster small solver (rtk_solve.cu), l <= 64 ------------------------------
 constexpr int kSolveLMax = 64;

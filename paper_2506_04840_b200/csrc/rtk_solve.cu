@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
                                                          const int* __restrict__ stop) {
   __shared__ double Ys[kRBr][kSL + 1];
   __shared__ double red[4][kSL][kRBr];
+  sm100::pdl_wait();   // the power step's Y partials
   if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kRBr;
@@ -847,6 +848,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   const int n = a.n, l = a.l;
   const int np = l * (l + 1) / 2;
   const int r0 = (int)((int64_t)rank * n / C), r1 = (int)((int64_t)(rank + 1) * n / C);
+  sm100::pdl_wait();   // the reduction's Y and Gram partials
   const double alpha0 = (a.step > 0) ? *a.alpha : 0.0;   // read before any cluster barrier
   const bool pve = a.pve_tol > 0.0 && a.step > 0;
   // Alg. B.1 stopped this mode at an earlier power step: the remaining launches are no-ops
@@ -1547,8 +1549,19 @@ size_t solve_gpart_doubles(int n, int l) { return (size_t)((n + kRBr - 1) / kRBr
 
 cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop) {
   const int nblk = (B.n + kRBr - 1) / kRBr;
-  reduce_gram_kernel<<<nblk, kST, 0, st>>>(B.Ypart, B.G, B.ltot, B.n_rows, B.n, B.l, B.Qd, B.alpha, power ? 1 : 0,
-                                           B.Y, B.gpart, stop);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblk, 1, 1);
+  cfg.blockDim = dim3(kST, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, reduce_gram_kernel, (const float*)B.Ypart, B.G, B.ltot, B.n_rows, B.n,
+                                     B.l, (const double*)B.Qd, (const double*)B.alpha, power ? 1 : 0, B.Y, B.gpart,
+                                     stop);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1577,13 +1590,15 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   cfg.blockDim = dim3(kST, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, step_kernel, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -382,6 +382,15 @@ static cudaError_t launch_rt(const TileArgs& a, TileOp op, int grid, int nt, siz
   return cudaGetLastError();
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RTK_PDL");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int num_sms() {
   static int v = 0;
   if (!v) {
