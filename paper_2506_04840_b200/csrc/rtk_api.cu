@@ -22,6 +22,17 @@ namespace {
 
 thread_local std::string g_err;
 
+// smallest unfolding width whose sketch runs on the fused engine (Omega planes precomputed) rather
+// than tc_op2 (Omega generated in shared memory); RTK_FUSED_SKETCH_MIN overrides (measurement)
+static int64_t fused_sketch_min() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("RTK_FUSED_SKETCH_MIN");
+    v = e ? atoll(e) : 100000;   // measured: C5 mode 2 (m = 5e4) faster on tc_op2, C3 mode 1 (1.6e5) fused
+  }
+  return v;
+}
+
 // ---- launch accounting / optional event profile (rtk_profile_begin/end) ----
 struct ProfRec {
   int kind, mode;
@@ -408,7 +419,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
       // sketch on the fused engine only for long unfoldings (Omega-plane generation has a fixed
       // cost; tc_op2 generates Omega in shared memory and is faster for small m)
-      if (fused && (step > 0 || v.m() >= 200000)) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
+      if (fused && (step > 0 || v.m() >= fused_sketch_min())) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
         int Gf = 0, rows = 0;
         const bool sk = step == 0;
         RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
