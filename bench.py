@@ -290,37 +290,58 @@ def run_ours(args, ws, rank, local):
                  for i, k in enumerate(["sketch", "power", "shrink", "small_solves"])}
 
     # ---- end to end through the public API from pinned host buffers ----
+    # Every step copies its input tensor host -> device (pinned, 4 GB at C5) and reads its result back
+    # device -> host inside the timed region.  The copies run on a copy stream into two device buffers:
+    # step i+1's H2D overlaps step i's solve (a data-loader style prefetch; the copy engine and the
+    # SMs work concurrently), and step i's solve waits for its own copy.
     e2e = None
     if not args.no_e2e:
         hostA = torch.empty_like(A, device="cpu").pin_memory()
         hostA.copy_(A)
-        Adev = torch.empty_like(A)
+        Adev = [torch.empty_like(A), torch.empty_like(A)]
         h_core = torch.empty(core.shape, dtype=torch.float32).pin_memory()
         h_U = [torch.empty(u.shape, dtype=torch.float32).pin_memory() for u in U]
         h2d = A.numel() * 4
         d2h = core.numel() * 4 + sum(u.numel() * 4 for u in U)
+        cstream = torch.cuda.Stream()
+        copied = [torch.cuda.Event(), torch.cuda.Event()]   # H2D into buffer b done
+        freed = [torch.cuda.Event(), torch.cuda.Event()]    # solve reading buffer b done
 
-        def e2e_step():
-            Adev.copy_(hostA, non_blocking=True)
-            rt.rsthosvd(Adev, ranks, p, q, seed, out=(core, U), workspace=work)
-            h_core.copy_(core, non_blocking=True)
-            for hu, u in zip(h_U, U):
-                hu.copy_(u, non_blocking=True)
+        def h2d_into(b):
+            cstream.wait_event(freed[b])
+            with torch.cuda.stream(cstream):
+                Adev[b].copy_(hostA, non_blocking=True)
+                copied[b].record(cstream)
 
-        e2e_step()
+        def e2e_run(k):
+            for b in range(2):
+                freed[b].record(stream)
+            h2d_into(0)
+            for i in range(k):
+                b = i % 2
+                if i + 1 < k:
+                    h2d_into(1 - b)          # next step's input, overlapping this step's solve
+                stream.wait_event(copied[b])
+                rt.rsthosvd(Adev[b], ranks, p, q, seed, out=(core, U), workspace=work)
+                freed[b].record(stream)
+                h_core.copy_(core, non_blocking=True)
+                for hu, u in zip(h_U, U):
+                    hu.copy_(u, non_blocking=True)
+
+        e2e_run(1)
         torch.cuda.synchronize()
         barrier(ws)
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         ke = max(1, min(args.steps, 5))
         f0.record(stream)
-        for _ in range(ke):
-            e2e_step()
+        e2e_run(ke)
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / ke, ws)
         e2e = {"value": e2e_ms / ws, "unit": "ms", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": ke}
+               "d2h_bytes_per_step": d2h, "steps": ke,
+               "overlap": "step i+1 H2D on a copy stream during step i's solve (2 device buffers)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
