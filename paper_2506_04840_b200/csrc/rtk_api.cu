@@ -429,16 +429,17 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
       } else {
+      const int G2 = tc_op2_grid(v, G);
       if (step == 0) {
-        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G, st, om));
+        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G2, st, om));
         g_launches += 1;
       } else {
         if (!fast) RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));   // else: written by step_kernel
         RTK_CK(tc_op1(v, l, planes, W, L.ldw, false, nullptr, 1, 1, 1, st, G));
-        RTK_CK(tc_op2(v, l, W, L.ldw, false, 0, 0, B.Ypart, G, st));
+        RTK_CK(tc_op2(v, l, W, L.ldw, false, 0, 0, B.Ypart, G2, st));
         g_launches += 3;
       }
-      B.G = G; B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
+      B.G = G2; B.ltot = tc_npad(l); B.n_rows = ((n + 127) / 128) * 128;
       }
     } else {
     TileLaunch T;

@@ -111,6 +111,7 @@ cudaError_t a2_finish(const float* B, int d, const int* l, const int* r, const i
 
 // ---- tcgen05 3xTF32 path (rtk_tc.cu) -------------------------------------------
 int tc_npad(int l);                                   // l padded to the UMMA N (16..64), 0 if > 64
+int tc_op2_grid(const View& v, int G);   // split-K grid of tc_op2 (<= K chunks)
 bool tc_supported(const View& v, int l);              // contiguous column-major view, sm_100
 cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* planes, cudaStream_t st);
 cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,

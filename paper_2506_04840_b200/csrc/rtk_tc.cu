@@ -527,6 +527,13 @@ cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t 
   }
 }
 
+// split-K CTAs of op2 for a grid of G: no more than the K chunks (an idle CTA would still write a
+// zero Y partial that the reduction then reads)
+int tc_op2_grid(const View& v, int G) {
+  const int64_t nkc = (v.m() + kBK - 1) / kBK;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(G, nkc));
+}
+
 // op2: Ypart[G][N][nit*128] = per-CTA partial M W (or M Omega_k when sketch)
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
                    float* Ypart, int G, cudaStream_t st, const float* om) {
