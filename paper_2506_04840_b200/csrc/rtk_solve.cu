@@ -610,7 +610,7 @@ __device__ void all_eigs(const double* d, const double* e, const double* e2, int
     int k = 0;
     if (c < l) {
       const double lo = blo[c], hi = bhi[c];
-      mu = lo + (hi - lo) * (double)(part + 1) / 5.0;
+      mu = lo + (hi - lo) * (0.2 * (double)(part + 1));   // same expression as the update below
       k = sturm_count(d, e2, l, mu);
     }
     cnt[tid] = k;
@@ -621,7 +621,7 @@ __device__ void all_eigs(const double* d, const double* e, const double* e2, int
       const double base = lo;
       const double w = hi - lo;
       for (int s = 0; s < 4; ++s) {
-        const double m = base + w * (double)(s + 1) / 5.0;
+        const double m = base + w * (0.2 * (double)(s + 1));
         if (cnt[4 * c + s] <= c) lo = fmax(lo, m);
         else hi = fmin(hi, m);
       }
