@@ -654,24 +654,28 @@ __device__ void tri_eigvecs(const double* d, const double* e, const double* lam,
     }
     for (int it = 0; it < 2; ++it) {
       // forward: u_i = d_i - lam - m_i e_{i-1},  m_i = e_{i-1}/u_{i-1};  y_i = x_i - m_i y_{i-1}
+      // (Lu keeps 1/u_i: one reciprocal on the forward chain, none on the backward one; rcp_fast is
+      // within an ulp, which inverse iteration does not notice)
       double u = d[0] - lm;
       if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
-      Lu[c] = u;
+      double ru = rcp_fast(u);
+      Lu[c] = ru;
       double y = Z[c];
       for (int i = 1; i < l; ++i) {
-        const double m = e[i - 1] / u;
+        const double m = e[i - 1] * ru;
         u = d[i] - lm - m * e[i - 1];
         if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
-        Lu[i * kLD + c] = u;
+        ru = rcp_fast(u);
+        Lu[i * kLD + c] = ru;
         y = Z[i * kLD + c] - m * y;
         Z[i * kLD + c] = y;
       }
       // back: x_{l-1} = y_{l-1}/u_{l-1};  x_i = (y_i - e_i x_{i+1}) / u_i
-      double x = Z[(l - 1) * kLD + c] / Lu[(l - 1) * kLD + c];
+      double x = Z[(l - 1) * kLD + c] * Lu[(l - 1) * kLD + c];
       Z[(l - 1) * kLD + c] = x;
       double mx = fabs(x);
       for (int i = l - 2; i >= 0; --i) {
-        x = (Z[i * kLD + c] - e[i] * x) / Lu[i * kLD + c];
+        x = (Z[i * kLD + c] - e[i] * x) * Lu[i * kLD + c];
         Z[i * kLD + c] = x;
         mx = fmax(mx, fabs(x));
       }
