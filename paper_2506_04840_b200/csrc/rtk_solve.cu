@@ -410,13 +410,15 @@ __device__ void tridiag_t(const double* A, int l, double* Hv, double* hb, double
       double s = (s0 + s1) + (s2 + s3);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      double uq = 0.0;   // (QH v)_i
+      double uq = 0.0;   // (QH v)_i, in 4 partial sums (a 16-FMA chain otherwise)
       if (ACC) {
+        double u4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int j = part + 4 * jj;
-          if (j > k && j < l) uq = fma(qh[jj], v[j], uq);
+          if (j > k && j < l) u4[jj & 3] = fma(qh[jj], v[j], u4[jj & 3]);
         }
+        uq = (u4[0] + u4[1]) + (u4[2] + u4[3]);
         uq += __shfl_xor_sync(0xffffffffu, uq, 1);
         uq += __shfl_xor_sync(0xffffffffu, uq, 2);
       }

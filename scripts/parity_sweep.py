@@ -66,6 +66,7 @@ def main():
     n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
     fails = 0
+    ties = 0
     done = 0
     while done < n_cases:
         c = case(rng)
@@ -100,12 +101,37 @@ def main():
                 if ranks[k] > cols:
                     gaps[k] = 0.0   # null-space completion: any orthonormal choice is valid
         orth = max(metrics.orthonormality(u) for u in gU)
-        ang = max([metrics.max_principal_angle(uo, ug) for uo, ug, gp in zip(orc.factors, gU, gaps) if gp > 0.1]
-                  or [0.0])
-        ok = abs(re_g - re_o) <= 1e-4 * re_o + 1e-7 and orth <= 1e-5 and ang <= 1e-3
+
+        def check(o):
+            re_o = metrics.relative_error(a, o.core, o.factors)
+            ang = max([metrics.max_principal_angle(uo, ug) for uo, ug, gp in zip(o.factors, gU, gaps) if gp > 0.1]
+                      or [0.0])
+            return abs(re_g - re_o) <= 1e-4 * re_o + 1e-7 and orth <= 1e-5 and ang <= 1e-3, re_o, ang
+
+        ok, re_o, ang = check(orc)
+        tag = "ok  " if ok else "FAIL"
+        if not ok and c["algo"] == "st":
+            # C6's residual risk: a column of an earlier U_k whose sign pivot is not determined at
+            # the precision of the data (top-two |entries| closer than the column's own GPU/oracle
+            # difference) may carry the other sign on the GPU; ST then feeds that sign to every later
+            # mode.  Both signs are valid outputs: re-run the oracle with the GPU's sign there.
+            flip = {}
+            for k in range(len(dims) - 1):
+                uo, ug = orc.factors[k], gU[k].astype(np.float64)
+                for j in range(uo.shape[1]):
+                    if float(np.dot(uo[:, j], ug[:, j])) < -0.99:
+                        col = np.sort(np.abs(uo[:, j]))[::-1]
+                        amb = col.size > 1 and (col[0] - col[1]) <= 20 * (float(np.max(np.abs(uo[:, j] + ug[:, j]))) + 1e-5 * col[0])
+                        if amb:
+                            flip.setdefault(k, []).append(j)
+            if flip:
+                ok, re_o, ang = check(fn(a, ranks, c["p"], c["q"], 5, shift=c["shift"], omega_kind=c["omega"],
+                                         flip=flip))
+                tag = "TIE " if ok else "FAIL"
+                ties += 1 if ok else 0
         fails += 0 if ok else 1
-        print(("ok  " if ok else "FAIL"), c, f"RE {re_g:.6e}/{re_o:.6e} orth {orth:.1e} angle {ang:.1e}", flush=True)
-    print(f"{done - fails}/{done} cases within tolerance")
+        print(tag, c, f"RE {re_g:.6e}/{re_o:.6e} orth {orth:.1e} angle {ang:.1e}", flush=True)
+    print(f"{done - fails}/{done} cases within tolerance ({ties} after re-pinning an undetermined sign, C6)")
     sys.exit(1 if fails else 0)
 
 

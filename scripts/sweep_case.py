@@ -30,8 +30,10 @@ for path in ["ffma", "tc"]:
     os.environ["RTK_PATH"] = path
     A = torch.from_numpy(np.asfortranarray(a)).cuda()
     seq = c["algo"] != "t"
-    g_core, g_U, rep = rt.solve(A, ranks, c["p"], c["q"], 5, sequential=seq, shift=c["shift"], report=True)
-    orc = tucker.rsthosvd(a, ranks, c["p"], c["q"], 5, shift=c["shift"])
+    g_core, g_U, rep = rt.solve(A, ranks, c["p"], c["q"], 5, sequential=seq, shift=c["shift"], report=True,
+                                omega_kind=c.get("omega", 0))
+    ofn = tucker.rsthosvd if seq else tucker.rthosvd
+    orc = ofn(a, ranks, c["p"], c["q"], 5, shift=c["shift"], omega_kind=c.get("omega", 0))
     gU = [u.cpu().numpy() for u in g_U]
     gaps = metrics.mode_gaps(a, ranks, orc.factors, seq)
     print(path, "gaps", np.round(gaps, 4), "angles", [f"{metrics.max_principal_angle(uo, ug):.2e}" for uo, ug in zip(orc.factors, gU)])

@@ -476,3 +476,24 @@ def test_a2_rank_above_unfolding_columns():
     for k, u in enumerate(res.factors):
         g = tucker.mode_product(g, u.T, k)
     np.testing.assert_allclose(res.core, g, atol=1e-10)
+
+
+def test_flip_hook_is_a_pure_sign_change():
+    """The parity harness's C6 near-tie hook: flip={} equals no flip; flipping a column of the
+    last mode's U_d negates that column and the matching core slice and nothing else (no later
+    mode sees it), so the Tucker approximation and its RE are unchanged."""
+    rng = np.random.default_rng(11)
+    dims, ranks = (12, 10, 9), (3, 4, 2)
+    core = rng.standard_normal((5, 5, 4))
+    a = tucker_tensor(core, [orthonormal_factor(n, 5 if n > 9 else 4, rng) for n in dims], noise=1e-2, rng=rng)
+    base = tucker.rsthosvd(a, ranks, 2, 2, 3)
+    same = tucker.rsthosvd(a, ranks, 2, 2, 3, flip={})
+    for u, v in zip(base.factors, same.factors):
+        assert np.array_equal(u, v)
+    fl = tucker.rsthosvd(a, ranks, 2, 2, 3, flip={2: [1]})
+    assert np.array_equal(fl.factors[0], base.factors[0]) and np.array_equal(fl.factors[1], base.factors[1])
+    assert np.array_equal(fl.factors[2][:, 1], -base.factors[2][:, 1])
+    assert np.array_equal(fl.factors[2][:, 0], base.factors[2][:, 0])
+    assert np.allclose(fl.core[:, :, 1], -base.core[:, :, 1], rtol=0, atol=1e-12)
+    assert np.allclose(fl.core[:, :, 0], base.core[:, :, 0], rtol=0, atol=1e-12)
+    assert abs(metrics.relative_error(a, fl.core, fl.factors) - metrics.relative_error(a, base.core, base.factors)) < 1e-12
