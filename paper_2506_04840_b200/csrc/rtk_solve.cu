@@ -1401,6 +1401,27 @@ __global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict
 
 // U(:, cc) = s Q_k V(:, cc) with the sign pin s (largest |entry| positive, lowest row on ties,
 // SPEC.md:232); V(:, cc) *= s so that the core keeps G = A x_k U_k^T.  One CTA per column.
+// u_i = sum_j Q(i, j) V(j, cc) for this thread's rows i = tid + t kST, t < kUR, in registers: the
+// loads of one j for all rows are independent (the sum itself runs in j order, as in the scalar form)
+constexpr int kUR = 8;
+__device__ __forceinline__ void a2_u_rows(const double* __restrict__ Q, int n, int l, const double* vs,
+                                          double (&u)[kUR]) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int t = 0; t < kUR; ++t) u[t] = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < l; ++j) {
+    const double v = vs[j];
+#pragma unroll
+    for (int t = 0; t < kUR; ++t) {
+      const int i = tid + t * kST;
+      if (i < n) u[t] = fma(Q[i + (int64_t)n * j], v, u[t]);
+    }
+  }
+}
+
+// U(:, cc) = Q V(:, cc) with the sign pin (C6, tie-tolerant pivot), V's column takes the same sign.
+// n <= kUR kST rows: each row's u is formed once in registers; larger n recompute it per pass.
 __global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q, int n, int l,
                                                    double* __restrict__ V, int r, float* __restrict__ U) {
   __shared__ double vs[kSL];
@@ -1409,13 +1430,31 @@ __global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q,
   const int cc = blockIdx.x, tid = threadIdx.x;
   if (tid < l) vs[tid] = V[tid + (int64_t)l * cc];
   __syncthreads();
-  double best = -1.0, bval = 0.0;
-  int bidx = 0x7fffffff;
-  for (int i = tid; i < n; i += kST) {
+  const bool reg = n <= kUR * kST;
+  double ur[kUR];
+  if (reg) a2_u_rows(Q, n, l, vs, ur);
+  auto urow = [&](int i) -> double {   // large-n mode: recompute
     double u = 0.0;
     for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+    return u;
+  };
+  // visit every row of this thread in ascending order with its u (registers, or recomputed)
+  auto rows = [&](auto&& f) {
+    if (reg) {
+#pragma unroll
+      for (int t = 0; t < kUR; ++t)
+        if (tid + t * kST < n && !f(tid + t * kST, ur[t])) return;
+    } else {
+      for (int i = tid; i < n; i += kST)
+        if (!f(i, urow(i))) return;
+    }
+  };
+  double best = -1.0, bval = 0.0;
+  int bidx = 0x7fffffff;
+  rows([&](int i, double u) {
     if (fabs(u) > best) { best = fabs(u); bidx = i; bval = u; }
-  }
+    return true;
+  });
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1434,11 +1473,10 @@ __global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q,
     piv_s = 0x7fffffff;
   }
   __syncthreads();
-  for (int i = tid; i < n; i += kST) {   // lowest row whose |u_i| reaches the tie threshold
-    double u = 0.0;
-    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
-    if (fabs(u) >= thr_s) { atomicMin(&piv_s, i); break; }
-  }
+  rows([&](int i, double u) {   // lowest row whose |u_i| reaches the tie threshold
+    if (fabs(u) >= thr_s) { atomicMin(&piv_s, i); return false; }
+    return true;
+  });
   __syncthreads();
   if (tid == 0) {
     double u = 0.0;
@@ -1448,11 +1486,10 @@ __global__ void __launch_bounds__(kST) a2_u_kernel(const double* __restrict__ Q,
   }
   __syncthreads();
   const double sgn = sgn_s;
-  for (int i = tid; i < n; i += kST) {
-    double u = 0.0;
-    for (int j = 0; j < l; ++j) u = fma(Q[i + (int64_t)n * j], vs[j], u);
+  rows([&](int i, double u) {
     U[i + (int64_t)n * cc] = (float)(sgn * u);
-  }
+    return true;
+  });
   if (tid < l) V[tid + (int64_t)l * cc] = sgn * vs[tid];
 }
 
