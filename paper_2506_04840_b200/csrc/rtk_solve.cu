@@ -1357,8 +1357,22 @@ __global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict
     const int i = idx % c, cc = idx / c;
     S.R[i * kLD + cc] = Z[i * kLD + (c - 1 - cc)];
   }
+  // Gram-Schmidt only where inverse iteration may not return orthonormal vectors: a null eigenvalue
+  // among the r kept (below c eps lambda_max) or two kept eigenvalues closer than 1e-8 lambda_max
+  // (as the step kernel's second-pass rule, C20); otherwise QH Z is orthonormal to rounding
+  __shared__ int s_cgs;
+  if (tid == 0) {
+    const double lmax = S.lam[c - 1];
+    bool need = !(lmax > 0.0);
+    for (int cc = 0; cc < r && !need; ++cc) {
+      const double lk = S.lam[c - 1 - cc];
+      if (!(lk > c * DBL_EPSILON * lmax)) need = true;
+      if (cc + 1 < r && S.lam[c - 1 - cc] - S.lam[c - 2 - cc] < 1e-8 * lmax) need = true;
+    }
+    s_cgs = need ? 1 : 0;
+  }
   __syncthreads();
-  for (int cc = 0; cc < r; ++cc) {
+  for (int cc = 0; cc < r && s_cgs; ++cc) {
     // the eigenvector first; if Gram-Schmidt leaves (almost) nothing of it -- a duplicate from a
     // degenerate cluster, e.g. the null space when r_k exceeds the rank of the l-core's unfolding --
     // complete with the first unit vector e_i that keeps a quarter of its norm
