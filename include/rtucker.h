@@ -34,9 +34,28 @@
  * non-NULL the call synchronises the stream and fills the report.
  *
  * ERRORS.  Every function returns an rtk_status; nothing throws across the ABI.
- * All argument checks run before any launch; on a non-zero status no output is
- * written.  rtk_last_error() returns a thread-local message for the last
- * non-zero status of this thread.
+ * All argument checks run before any launch; on a non-zero status other than
+ * RTK_ERR_NUMERIC no output is written.  rtk_last_error() returns a thread-local
+ * message for the last non-zero status of this thread.
+ *
+ * NUMERIC FAILURES (RTK_ERR_NUMERIC).  A solve that meets a non-finite iterate or a
+ * Cholesky breakdown its basis completion cannot repair still writes its outputs
+ * (unreliable).  With a report (rep != NULL) that call returns RTK_ERR_NUMERIC and
+ * sets rep->numeric.  Without a report the call is asynchronous and cannot see its
+ * own result: the failure is latched in a per-device flag and the NEXT solver call
+ * on that device (once the failing solve has executed) returns RTK_ERR_NUMERIC
+ * without launching anything and clears the flag (CUDA sticky-error style).
+ *
+ * LIMITS.  n_k <= 4096 (tile kernels), l_k = r_k + p <= 96 (one-CTA small solves;
+ * l_k <= 64 takes the cluster small solver), Alg. A.2 and Alg. B.1 need l_k <= 64.
+ *
+ * STREAMING PATHS (chosen per mode, results equal up to rounding; rtk_options.path
+ * forces one).  tcgen05 3xTF32 when l_k <= 64, the unfolding is a contiguous
+ * column-major view (mode 1 of A, every Alg. 4 mode, since Alg. 4 writes each
+ * shrunk unfolding contiguously) whose leading dimension is a multiple of 4 and
+ * whose base is 16-byte aligned; then the fused single-HBM-pass engine when
+ * additionally n_k <= 1024.  Strided unfoldings (Alg. 3 modes >= 2), l_k > 64 and
+ * unaligned data use the FP32 FFMA tile kernels (bulk-copy row loads, no permute).
  */
 #ifndef RTUCKER_H
 #define RTUCKER_H
@@ -57,11 +76,13 @@ extern "C" {
 typedef enum rtk_status {
   RTK_OK = 0,
   RTK_ERR_ARG = 1,       /* NULL pointer; d < 2 or d > 8; n_k < 1; r_k not in [1,n_k]; p < 0; q < 1 */
-  RTK_ERR_SHAPE = 2,     /* l_k = r_k + p > min(n_k, m_k), or n_k > 2048 (kernel limit) */
+  RTK_ERR_SHAPE = 2,     /* l_k = r_k + p > min(n_k, m_k); n_k > 4096 or l_k > 96
+                          * (kernel limits); Alg. A.2 with l_k > 64; path = 2 where tcgen05 n/a */
   RTK_ERR_ALIGN = 3,     /* A not 4-byte aligned */
   RTK_ERR_WORKSPACE = 4, /* ws_bytes < rtk_workspace_bytes(...) */
   RTK_ERR_CUDA = 5,      /* launch / runtime error; message kept */
-  RTK_ERR_NUMERIC = 6    /* non-finite iterate or unrepairable Cholesky breakdown (reported via rep) */
+  RTK_ERR_NUMERIC = 6    /* non-finite iterate or unrepairable Cholesky breakdown: returned by the
+                          * call itself when rep != NULL, else by the next call (see above) */
 } rtk_status;
 
 /* Optional host-side report (SPEC ShiftTrace analogue).  Any pointer may be NULL. */

@@ -41,14 +41,6 @@ def mode_product(t: np.ndarray, b: np.ndarray, k: int) -> np.ndarray:
     return fold(out, k, dims)
 
 
-def reconstruct(core: np.ndarray, factors) -> np.ndarray:
-    """A_hat = G x_1 U_1 x_2 U_2 ... x_d U_d."""
-    t = np.asarray(core, dtype=np.float64)
-    for k, u in enumerate(factors):
-        t = mode_product(t, np.asarray(u, dtype=np.float64), k)
-    return t
-
-
 PIN_TIE = 1e-5
 
 
@@ -190,26 +182,19 @@ def rthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True,
 
 
 def rsthosvd(a: np.ndarray, ranks, p: int, q: int, seed: int, shift: bool = True,
-             pve=None, omega_kind: int = OMEGA_GAUSS, flip=None) -> Result:
+             pve=None, omega_kind: int = OMEGA_GAUSS) -> Result:
     """Alg. 4, shifted randomized ST-HOSVD, order (1..d).
 
     shift=False is Alg. 2's ST branch; pve=(tol, q_max) is Alg. B.1 (pinned by
     tests/test_oracle_tucker.py::test_pve_*: reductions to Alg. 4 at q_max and q = 1, the
     rank-l closed form sigma = lambda_i(M M^T), monotonicity in tol).
     G starts as A; mode k factors G_(k) then G = G x_k U_k^T (line 12).
-    flip={k: [j, ...]} (test harness only, None = off) negates the listed columns of U_k after
-    the sign pin: where a column's pivot is not determined at the precision of the data (C6's
-    residual near-tie), the other sign is an equally valid output and the later modes of the
-    ST recursion (which see U_k's signs through G) are compared under it.
     """
     g = np.asarray(a, dtype=np.float64)
     us, trs = [], []
     for k, r in enumerate(ranks):
         u, tr = _range_finder(unfold(g, k), r, p, q, seed, k + 1, shift, pve,
                               omega_kind=omega_kind, dims=g.shape)
-        if flip and k in flip:
-            u = u.copy()
-            u[:, list(flip[k])] *= -1.0
         us.append(u)
         trs.append(tr)
         g = mode_product(g, u.T, k)

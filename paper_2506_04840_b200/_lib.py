@@ -151,6 +151,30 @@ def workspace_bytes(sequential: bool, dims, ranks, p: int, q: int, variant: int 
     return int(n)
 
 
+def _check_outputs(core, U, dims, ranks, dev):
+    """out=(core, U) are written by the kernels through raw pointers: each U[k] must be an
+    n_k x r_k float32 column-major (stride(0) == 1, stride(1) == n_k) tensor on A's device, core
+    an r_1 x ... x r_d float32 column-major tensor on A's device (the ABI writes U[k] with leading
+    dimension n_k, so stride(1) must equal n_k)."""
+    import torch
+    if len(U) != len(dims):
+        raise ValueError("out: need one factor per mode")
+    for k, (u, n, r) in enumerate(zip(U, dims, ranks)):
+        if not isinstance(u, torch.Tensor) or u.dtype != torch.float32 or u.device != dev:
+            raise ValueError(f"out: U[{k}] must be a float32 tensor on {dev}")
+        if tuple(u.shape) != (n, r):
+            raise ValueError(f"out: U[{k}] has shape {tuple(u.shape)}, expected {(n, r)}")
+        if (n > 1 and u.stride(0) != 1) or (r > 1 and u.stride(1) != n):
+            raise ValueError(f"out: U[{k}] must be column-major with leading dimension n_k "
+                             "(stride(0) == 1, stride(1) == n_k)")
+    if not isinstance(core, torch.Tensor) or core.dtype != torch.float32 or core.device != dev:
+        raise ValueError(f"out: core must be a float32 tensor on {dev}")
+    if tuple(core.shape) != tuple(ranks):
+        raise ValueError(f"out: core has shape {tuple(core.shape)}, expected {tuple(ranks)}")
+    if not _is_column_major(core):
+        raise ValueError("out: core must be column-major (use as_column_major)")
+
+
 @dataclass
 class Report:
     alpha_trace: list      # d lists of q alphas
@@ -158,7 +182,6 @@ class Report:
     q_used: list
     fallback: int
     numeric: int
-    jacobi_sweeps: list = None   # sweeps of each mode's last Jacobi solve (diagnostics)
 
 
 class _WorkspaceCache:
@@ -212,10 +235,16 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
         core = as_column_major(torch.empty(ranks, dtype=torch.float32, device=dev))
     else:
         core, U = out
+        _check_outputs(core, U, dims, ranks, dev)
     dd = (ctypes.c_int64 * d)(*dims)
     rr = (ctypes.c_int32 * d)(*ranks)
     up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
     ws_bytes = workspace_bytes(sequential, dims, ranks, p, q, variant, omega_kind, path) if min(ranks) >= 1 else 0
+    if workspace is not None:
+        if not workspace.is_cuda or workspace.device != dev or not workspace.is_contiguous():
+            raise ValueError("workspace must be a contiguous CUDA tensor on A's device")
+        if workspace.numel() * workspace.element_size() < ws_bytes:
+            raise ValueError(f"workspace too small: need {ws_bytes} bytes")
     ws = workspace if workspace is not None else _WS.get(dev, max(ws_bytes, 1))
     opt = _Options(1 if sequential else 0, 1 if shift else 0, float(pve_tol), int(path), int(variant),
                    int(omega_kind))
@@ -232,7 +261,7 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     with torch.cuda.device(dev):
         code = lib.rtk_solve(ctypes.byref(opt), ctypes.c_void_p(A.data_ptr()), dd, d, rr, p, q,
                              ctypes.c_uint64(seed), up, ctypes.c_void_p(core.data_ptr()),
-                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_handle(dev),
+                             ctypes.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size(), _stream_handle(dev),
                              ctypes.byref(rep) if rep is not None else None)
     _check(code)
     if not report:
@@ -241,8 +270,7 @@ def solve(A, ranks, p: int, q: int, seed: int, sequential: bool = True, shift: b
     ls = [r + p for r in ranks]
     r_obj = Report([list(at[k * q:(k + 1) * q]) for k in range(d)],
                    [list(sg[k * 128:k * 128 + ls[k]]) for k in range(d)],
-                   list(qu), rep.fallback, rep.numeric,
-                   [[sg[k * 128 + 100 + s] for s in range(min(q + 1, 24))] for k in range(d)])
+                   list(qu), rep.fallback, rep.numeric)
     return core, U, r_obj
 
 

@@ -24,13 +24,9 @@ thread_local std::string g_err;
 
 // smallest unfolding width whose sketch runs on the fused engine (Omega planes precomputed) rather
 // than tc_op2 (Omega generated in shared memory); RTK_FUSED_SKETCH_MIN overrides (measurement)
-static int64_t fused_sketch_min() {
-  static int64_t v = -1;
-  if (v < 0) {
-    const char* e = getenv("RTK_FUSED_SKETCH_MIN");
-    v = e ? atoll(e) : 100000;   // measured: C5 mode 2 (m = 5e4) faster on tc_op2, C3 mode 1 (1.6e5) fused
-  }
-  return v;
+static int64_t fused_sketch_min() {   // read per call so that tests can switch it
+  const char* e = getenv("RTK_FUSED_SKETCH_MIN");
+  return e ? atoll(e) : 100000;   // measured: C5 mode 2 (m = 5e4) faster on tc_op2, C3 mode 1 (1.6e5) fused
 }
 
 // ---- launch accounting / optional event profile (rtk_profile_begin/end) ----
@@ -66,6 +62,34 @@ struct ProfScope {
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
+}
+
+// Sticky RTK_ERR_NUMERIC (include/rtucker.h): every solve ends with a one-thread kernel that sets a
+// per-device flag in mapped pinned host memory when any mode's status word reports a numeric
+// failure.  A call without a report cannot wait for its own result (it is asynchronous), so the
+// NEXT call on that device returns RTK_ERR_NUMERIC (and clears the flag) once the failing solve
+// has executed; a call with a report returns it directly.
+__global__ void numeric_flag_kernel(const int* status, int d, int* flag) {
+  int bad = 0;
+  for (int k = 0; k < d; ++k) bad |= (status[4 * k] != 0);
+  if (bad) *(volatile int*)flag = 1;
+}
+
+int* numeric_flag_host(int dev) {   // nullptr if the pinned allocation failed (check then skipped)
+  static int* flags[64] = {};
+  static std::mutex mu;
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!flags[dev]) {
+    int* h = nullptr;
+    if (cudaHostAlloc((void**)&h, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    *h = 0;
+    flags[dev] = h;
+  }
+  return flags[dev];
 }
 
 constexpr int kLMaxApi = 96;
@@ -185,6 +209,7 @@ struct Layout {
 Layout plan(const Problem& P, int nsm, const float* A, int path) {
   Layout L;
   size_t ypart = 0, nl = 0, qsz = 0, gp = 0, ll = 0, lmax = 0, planes = 0, wbuf = 0;
+  int wN = 0;   // largest padded N over the tcgen05 range modes
   L.sk.resize(P.d); L.pw.resize(P.d); L.sh.resize(P.d);
   L.tc_range.assign(P.d, 0);
   L.tc_shrink.assign(P.d, 0);
@@ -208,7 +233,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
       ypart = std::max(ypart, (size_t)nsm * N * nit * 128);
       planes = std::max(planes, (size_t)2 * N * pad4(rv.n));
       ldw = std::max<int64_t>(ldw, pad4(rv.m()));
-      wbuf = std::max(wbuf, (size_t)2 * N * pad4(rv.m()));
+      wN = std::max(wN, N);
     }
     if (L.tc_shrink[k]) planes = std::max(planes, (size_t)2 * tc_npad(P.keep[k]) * pad4(rv.n));
     L.sk[k] = plan_tile(rv, l, OP_SKETCH, nsm);
@@ -232,6 +257,10 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
       shr = std::max(shr, e);
     }
   }
+  // W (two-kernel path: 2N rows of W) and the fused sketch's Omega planes (2N rows) are both
+  // addressed with the common leading dimension ldw = max pad4(m_k): size for the largest N
+  // times that ldw, not per mode (a mode with a larger N but a smaller m would overrun)
+  wbuf = (size_t)2 * wN * (size_t)ldw;
   L.shr_elems = shr;
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off += align_up(std::max<size_t>(bytes, 16)); return o; };
@@ -572,6 +601,14 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (opt.path < 0 || opt.path > 2) return fail(RTK_ERR_ARG, "path must be 0 (auto), 1 (FFMA) or 2 (tcgen05)");
+  int dev = 0;
+  RTK_CK(cudaGetDevice(&dev));
+  int* nflag = numeric_flag_host(dev);
+  if (nflag && *(volatile int*)nflag) {
+    *(volatile int*)nflag = 0;
+    return fail(RTK_ERR_NUMERIC, "an earlier solve on this device hit a numeric failure (non-finite iterate or "
+                                 "unrepairable Cholesky breakdown); its outputs are unreliable");
+  }
   const Layout L = plan_cached(P, num_sms(), A, opt.path);
   if (opt.path == 2)
     for (int k = 0; k < d; ++k)
@@ -645,6 +682,14 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
       if (rc) return rc;
     }
   }
+  if (nflag) {
+    int* dflag = nullptr;
+    RTK_CK(cudaHostGetDevicePointer((void**)&dflag, nflag, 0));
+    numeric_flag_kernel<<<1, 1, 0, st>>>((const int*)(ws + L.status), d, dflag);
+    RTK_CK(cudaGetLastError());
+    g_launches += 1;
+  }
+  bool numeric = false;
   if (rep) {
     RTK_CK(cudaStreamSynchronize(st));
     std::vector<int> status((size_t)d * 4);
@@ -660,9 +705,14 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
       rep->fallback += status[4 * k + 1];
       if (status[4 * k]) rep->numeric = RTK_ERR_NUMERIC;
     }
+    numeric = rep->numeric != 0;
+    if (numeric && nflag) *(volatile int*)nflag = 0;   // reported now, not again at the next call
   }
   if (own) RTK_CK(cudaFreeAsync(ws, st));
   RTK_CK(cudaGetLastError());
+  if (numeric)
+    return fail(RTK_ERR_NUMERIC, "numeric failure (non-finite iterate or unrepairable Cholesky breakdown); "
+                                 "outputs written but unreliable");
   return RTK_OK;
 }
 

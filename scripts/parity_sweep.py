@@ -114,24 +114,29 @@ def main():
             # C6's residual risk: a column of an earlier U_k whose sign pivot is not determined at
             # the precision of the data (top-two |entries| closer than the column's own GPU/oracle
             # difference) may carry the other sign on the GPU; ST then feeds that sign to every later
-            # mode.  Both signs are valid outputs: re-run the oracle with the GPU's sign there.
-            flip = {}
+            # mode, which then draws effectively different sketches.  Such a case is reported as
+            # undetermined, never re-run with a GPU-chosen sign: only what the sign cannot change is
+            # compared (orthonormality everywhere, principal angles of modes up to the ambiguous one).
+            k_amb = None
             for k in range(len(dims) - 1):
                 uo, ug = orc.factors[k], gU[k].astype(np.float64)
                 for j in range(uo.shape[1]):
                     if float(np.dot(uo[:, j], ug[:, j])) < -0.99:
                         col = np.sort(np.abs(uo[:, j]))[::-1]
-                        amb = col.size > 1 and (col[0] - col[1]) <= 20 * (float(np.max(np.abs(uo[:, j] + ug[:, j]))) + 1e-5 * col[0])
-                        if amb:
-                            flip.setdefault(k, []).append(j)
-            if flip:
-                ok, re_o, ang = check(fn(a, ranks, c["p"], c["q"], 5, shift=c["shift"], omega_kind=c["omega"],
-                                         flip=flip))
-                tag = "TIE " if ok else "FAIL"
+                        if col.size > 1 and (col[0] - col[1]) <= 20 * (float(np.max(np.abs(uo[:, j] + ug[:, j])))
+                                                                       + 1e-5 * col[0]):
+                            k_amb = k if k_amb is None else min(k_amb, k)
+            if k_amb is not None:
+                ang = max([metrics.max_principal_angle(uo, ug)
+                           for kk, (uo, ug, gp) in enumerate(zip(orc.factors, gU, gaps)) if kk <= k_amb and gp > 0.1]
+                          or [0.0])
+                ok = orth <= 1e-5 and ang <= 1e-3
+                tag = "UNDET" if ok else "FAIL"
                 ties += 1 if ok else 0
         fails += 0 if ok else 1
         print(tag, c, f"RE {re_g:.6e}/{re_o:.6e} orth {orth:.1e} angle {ang:.1e}", flush=True)
-    print(f"{done - fails}/{done} cases within tolerance ({ties} after re-pinning an undetermined sign, C6)")
+    print(f"{done - fails}/{done} cases within tolerance ({ties} with an undetermined sign pivot, C6: "
+          "sign-invariant checks only)")
     sys.exit(1 if fails else 0)
 
 

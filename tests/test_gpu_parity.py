@@ -33,7 +33,45 @@ def run_both(a, ranks, p, q, seed, sequential, shift=True):
     return g_core, g_U, rep, orc
 
 
-def check(a, ranks, p, q, seed, sequential, gaps=None, alpha_rtol=1e-3):
+# Element-wise comparison (both sides sign-pinned, C6).  The GPU and the oracle run the same
+# iteration on the same Omega; they differ by the fp32 stream's rounding, a relative perturbation
+# eps of each iterate Y.  A singular vector u_i of the last Y then moves by about
+# eps * sigma_1 / delta_i with delta_i = min_{j != i} |sigma_i - sigma_j| (first-order perturbation
+# of an isolated singular vector), so column i is compared where that bound is informative
+# (<= 1e-3) with EW_EPS = 1e-5 (fp32 rounding ~6e-8 per operation, grown over K-long sums and q+1
+# passes; 10x the measured worst case).  The core is compared element-wise against the fp64 mode
+# products of the GPU's OWN factors (A x_1 U_1^T ... x_d U_d^T), which checks the shrink / core
+# kernels entry by entry independently of how well the factors are determined.
+EW_EPS = 1e-5
+
+
+def elementwise_checks(a, g_core, g_U, orc, min_cols=0):
+    checked = 0
+    worst = 0.0
+    for k, (ug, uo) in enumerate(zip(g_U, orc.factors)):
+        sig = np.asarray(orc.traces[k].sigma[-1], dtype=np.float64)
+        for i in range(uo.shape[1]):
+            others = np.delete(sig, i)
+            delta = np.min(np.abs(sig[i] - others)) if others.size else sig[0]
+            tol = EW_EPS * sig[0] / max(delta, 1e-300)
+            if tol > 1e-3:
+                continue
+            err = float(np.max(np.abs(ug[:, i].astype(np.float64) - uo[:, i])))
+            worst = max(worst, err / tol)
+            assert err <= tol, (k, i, err, tol)
+            checked += 1
+    assert checked >= min_cols, (checked, min_cols)
+    ref = np.asarray(a, dtype=np.float64)
+    for k, u in enumerate(g_U):
+        ref = tucker.mode_product(ref, u.astype(np.float64).T, k)
+    cerr = float(np.max(np.abs(g_core.astype(np.float64) - ref)))
+    assert cerr <= 1e-5 * float(np.max(np.abs(ref))), (cerr, float(np.max(np.abs(ref))))
+    print(f"elementwise: {checked} factor columns, worst err/tol {worst:.3f}, core max err "
+          f"{cerr / max(float(np.max(np.abs(ref))), 1e-300):.2e} of max|core|")
+    return checked
+
+
+def check(a, ranks, p, q, seed, sequential, gaps=None, alpha_rtol=1e-3, ew_cols=None):
     g_core, g_U, rep, orc = run_both(a, ranks, p, q, seed, sequential)
     assert rep.numeric == 0
     re_g = metrics.relative_error(a, g_core, g_U)
@@ -49,7 +87,14 @@ def check(a, ranks, p, q, seed, sequential, gaps=None, alpha_rtol=1e-3):
     for k, tr in enumerate(orc.traces):
         if tr.alpha and max(tr.alpha) > 0:
             np.testing.assert_allclose(rep.alpha_trace[k], tr.alpha, rtol=alpha_rtol, atol=1e-12)
+    if ew_cols is not None:
+        elementwise_checks(a, g_core, g_U, orc, min_cols=ew_cols)
     return re_g, re_o
+
+
+# C1 (gapped Gaussian core) and C4 (exponential decay) have well separated leading singular
+# values: every factor column of C1 and most of C4 are determined to fp32 and compared entry-wise
+EW_COLS = {"c1": 15, "c2": 0, "c3": 0, "c4": 20}
 
 
 @pytest.mark.parametrize("path", ["ffma", "tc", "fused"])
@@ -59,7 +104,47 @@ def test_config_parity(cfg, path, monkeypatch):
     monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
     c = CONFIGS[cfg]
     a = make_config_tensor(cfg)
-    check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], c["algo"] == "rsthosvd")
+    check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], c["algo"] == "rsthosvd", ew_cols=EW_COLS[cfg])
+
+
+@pytest.mark.parametrize("seq", [False, True])
+@pytest.mark.parametrize("dims,ranks,p,q", [
+    ((640, 40, 36), (20, 8, 6), 6, 3),        # n_1 > 512: 2-CTA cluster
+    ((1000, 30, 20), (30, 6, 5), 10, 2),      # n_1 = 1000, l = 40
+    ((1000, 64, 40), (50, 10, 8), 10, 3),     # n_1 = 1000, l = 60 (N = 64): C5's mode-1 kernel shape
+])
+def test_fused_sketch_engine(seq, dims, ranks, p, q, monkeypatch):
+    """The fused Omega-plane sketch (the engine C5's mode 1 sketch runs on, normally only for
+    m >= 1e5) forced on at small m with RTK_FUSED_SKETCH_MIN=0: oracle parity incl. alpha traces."""
+    monkeypatch.setenv("RTK_FUSED_SKETCH_MIN", "0")
+    rng = np.random.default_rng(sum(dims) + 101)
+    cr = tuple(min(n, r + 3) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
+    us = [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)]
+    a = tucker_tensor(core, us, noise=1e-3, rng=rng)
+    check(a, ranks, p, q, 77, seq, alpha_rtol=5e-3, ew_cols=0)
+
+
+def test_c5_launch_path_ci_size():
+    """C5's recipe and parameters (r = 50, p = 10, q = 5) at 1000 x 400 x 300: mode 1 is n = 1000,
+    l = 60, m = 1.2e5 >= 1e5, so the sketch takes the fused Omega-plane engine on the 2-CTA
+    cluster and the power steps the fused engine, exactly C5 mode 1's launch configuration;
+    full oracle parity (RE, orthonormality, alpha traces, gated angles, core entries)."""
+    c = CONFIGS["c5"]
+    a = make_config_tensor("c5", dims=(1000, 400, 300))
+    check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], True, ew_cols=0)
+
+
+def test_wide_mode_after_narrow_workspace():
+    """Workspace regression (W / Omega-plane buffer sized for the largest N times the common
+    leading dimension): mode 1 has the larger N (l = 60) but the smaller m (1.04e5, fused sketch),
+    mode 2 the larger m (1.3e5) with l = 30."""
+    rng = np.random.default_rng(2600)
+    dims, ranks = (1000, 40, 2600), (50, 20, 20)
+    cr = (64, 24, 24)
+    core = rng.standard_normal(cr) * np.exp(-0.1 * np.indices(cr).sum(axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    check(a, ranks, 10, 2, 41, True, alpha_rtol=5e-3)
 
 
 @pytest.mark.parametrize("seq", [False, True])
@@ -386,12 +471,12 @@ def test_a2_rank_exceeds_core_rank():
 
 
 # ------------------------------------------------------------ C5 at full size (the bench's launch)
-def test_c5_full_size_properties():
-    """BASELINE C5 (1000^3, r = 50, p = 10, q = 5) through the public API exactly as bench.py runs
-    it, checked where the float64 oracle cannot follow at this size: sampled core entries recomputed
-    one by one in fp64 from the factors, the core identity ||A||^2 - ||core||^2 = ||A - A_hat||^2,
-    orthonormal factors, alpha monotone and below lambda_l(A_(1) A_(1)^T)/2, and
-    mode 1's projection error within 1 % of the optimum from the exact Gram eigenvalues."""
+def test_c5_full_size_vs_oracle():
+    """BASELINE C5 (1000^3 fp32, r = 50, p = 10, q = 5) through the public API exactly as bench.py
+    runs it (same tensor, same Omega seed, same launch configuration), against oracle.rsthosvd in
+    float64 on the host copy of that very tensor (~20 GB of host RAM, tens of seconds): RE within
+    1e-4 relative, orthonormality <= 1e-5, alpha traces at rtol 1e-3, principal angles where the
+    oracle's gap exceeds 10 %, core entries against the fp64 mode products of the GPU factors."""
     torch = cuda_or_skip()
     from paper_2506_04840_b200 import rsthosvd
     from workloads import make_config_tensor_torch
@@ -399,39 +484,24 @@ def test_c5_full_size_properties():
     A = make_config_tensor_torch("c5")                      # (1000, 1000, 1000) column-major fp32
     core, U, rep = rsthosvd(A, c["ranks"], c["p"], c["q"], c["omega_seed"], report=True)
     torch.cuda.synchronize()
+    g_core, g_U = core.cpu().numpy(), [u.cpu().numpy() for u in U]
+    a = A.cpu().numpy()                                     # Fortran-ordered view of the same bytes
+    del A
+    torch.cuda.empty_cache()
+    assert a.flags.f_contiguous
+    orc = tucker.rsthosvd(a, c["ranks"], c["p"], c["q"], c["omega_seed"])
     assert rep.numeric == 0
-    Ud = [u.double() for u in U]
-    for u in Ud:
-        assert torch.linalg.matrix_norm(u.T @ u - torch.eye(u.shape[1], device=u.device, dtype=torch.float64)) <= ORTH_TOL
-    # A_(1)^T as a (n2 n3) x n1 view (rows of the C-contiguous (n3, n2, n1) tensor)
-    X = A.permute(2, 1, 0).reshape(-1, A.shape[0])
-    n1 = A.shape[0]
-    G = torch.zeros((n1, n1), dtype=torch.float64, device=A.device)
-    for s0 in range(0, X.shape[0], 100000):
-        xc = X[s0:s0 + 100000].double()
-        G += xc.T @ xc
-    lam = torch.linalg.eigvalsh(G).flip(0)                 # descending
-    l = c["ranks"][0] + c["p"]
-    al = [0.0] + list(rep.alpha_trace[0])
-    assert all(b >= a0 for a0, b in zip(al, al[1:]))
-    assert max(rep.alpha_trace[0]) <= lam[l - 1].item() / 2 * (1 + 1e-6)
-    r1 = c["ranks"][0]
-    opt = lam[r1:].sum().item()
-    proj = (torch.trace(G) - torch.trace(Ud[0].T @ G @ Ud[0])).item()
-    assert opt <= proj <= 1.01 * opt, (proj, opt)
-    # sampled core entries, one by one: core[a,b,c] = sum A[i,j,k] U1[i,a] U2[j,b] U3[k,c]
-    g = torch.Generator(device="cpu").manual_seed(3)
-    idx = [tuple(int(torch.randint(0, r, (1,), generator=g)) for r in c["ranks"]) for _ in range(6)]
-    for (a_, b_, c_) in idx:
-        t = torch.zeros((), dtype=torch.float64, device=A.device)
-        for k0 in range(0, A.shape[2], 100):
-            slab = A[:, :, k0:k0 + 100].double()
-            t += torch.einsum("ijk,i,j,k->", slab, Ud[0][:, a_], Ud[1][:, b_], Ud[2][k0:k0 + 100, c_])
-        ref = t.item()
-        got = core[a_, b_, c_].item()
-        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)) + 1e-6 * core.abs().max().item(), ((a_, b_, c_), got, ref)
-    # core identity for orthonormal factors: ||A - A_hat||^2 = ||A||^2 - ||core||^2
-    a2 = sum((A[:, :, k0:k0 + 100].double() ** 2).sum().item() for k0 in range(0, A.shape[2], 100))
-    c2 = (core.double() ** 2).sum().item()
-    re = ((a2 - c2) / a2) ** 0.5
-    assert 0.94 < re < 0.97, re                              # RE ~ 0.955 for this recipe
+    re_g = metrics.relative_error(a, g_core, g_U)
+    re_o = metrics.relative_error(a, orc.core, orc.factors)
+    print(f"C5 full size: RE gpu {re_g:.9e} oracle {re_o:.9e} rel diff {abs(re_g - re_o) / re_o:.2e}")
+    assert abs(re_g - re_o) <= RE_TOL * re_o, (re_g, re_o)
+    for k, tr in enumerate(orc.traces):
+        np.testing.assert_allclose(rep.alpha_trace[k], tr.alpha, rtol=1e-3, atol=1e-12)
+    for u in g_U:
+        assert metrics.orthonormality(u) <= ORTH_TOL
+    gaps = metrics.mode_gaps(a, c["ranks"], orc.factors, True)
+    print("C5 gaps", gaps)
+    for k, u in enumerate(g_U):
+        if gaps[k] > 0.10:
+            assert metrics.max_principal_angle(orc.factors[k], u) <= ANGLE_TOL, (k, gaps[k])
+    elementwise_checks(a, g_core, g_U, orc)

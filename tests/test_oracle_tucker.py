@@ -88,6 +88,52 @@ def test_principal_angle_known_rotation():
     assert metrics.max_principal_angle(u, u @ np.array([[0.6, 0.8], [-0.8, 0.6]])) < 1e-15
 
 
+def _known_sv_matrix(sig, n, m, seed):
+    """n x m matrix with singular values sig (descending), random orthonormal singular vectors."""
+    rng = np.random.default_rng(seed)
+    k = len(sig)
+    return orthonormal_factor(n, k, rng) @ np.diag(sig) @ orthonormal_factor(m, k, rng).T
+
+
+@pytest.mark.parametrize("n,m", [(5, 9), (9, 5)])
+def test_spectral_gap_known_singular_values(n, m):
+    """gap_r = (sigma_r - sigma_{r+1}) / sigma_r on matrices with known sigma.
+    Probes: an off-by-one (w[r] vs w[r-1]) gives 0.1 instead of 0.375 at r = 2; working on the
+    eigenvalues lambda = sigma^2 instead of sigma gives 0.609; a wide/tall transpose slip changes
+    nothing only if the implementation is right for both shapes."""
+    sig = np.array([10.0, 8.0, 5.0, 4.5, 1.0])
+    a = _known_sv_matrix(sig, n, m, 11)
+    assert abs(metrics.spectral_gap(a, 1) - 0.2) < 1e-12
+    assert abs(metrics.spectral_gap(a, 2) - 0.375) < 1e-12
+    assert abs(metrics.spectral_gap(a, 3) - 0.1) < 1e-12
+    # sigma_6 = 0 (rank 5): the Gram's zero eigenvalues are rounding noise ~ eps lambda_1, whose
+    # square root is ~1e-7 sigma_1, so the gap is 1 to that accuracy
+    assert abs(metrics.spectral_gap(a, 5) - 1.0) < 1e-6
+
+
+def test_spectral_gap_rank_deficient_and_full():
+    sig = np.array([3.0, 2.0])
+    a = _known_sv_matrix(sig, 6, 7, 12)
+    assert abs(metrics.spectral_gap(a, 2) - 1.0) < 1e-6             # sigma_3 = 0: full gap
+    assert metrics.spectral_gap(np.eye(4), 4) == 1.0                 # r = n: nothing discarded
+
+
+def test_mode_gaps_orthogonally_decomposable_tensor():
+    """A = sum_i s_i u_i o v_i o w_i with orthonormal u, v, w: every unfolding has singular values
+    s (T-HOSVD gaps in closed form).  ST with U_1 = [u_1..u_3], U_2 = [v_1, v_2]: G_(2) keeps
+    s_1..s_3 and G_(3) keeps s_1, s_2, so mode 3's gap at r = 2 is 1 (sigma_3 = 0) - it would be
+    0.25 if mode_gaps read A instead of the shrunk G (pins the ST recursion and its factors)."""
+    rng = np.random.default_rng(13)
+    s = np.array([5.0, 4.0, 3.0, 2.0, 1.0, 0.5])
+    dims = (9, 8, 7)
+    f = [orthonormal_factor(n, len(s), rng) for n in dims]
+    a = np.einsum("i,ai,bi,ci->abc", s, *f)
+    gt = metrics.mode_gaps(a, (2, 3, 4), None, sequential=False)
+    np.testing.assert_allclose(gt, [(4 - 3) / 4, (3 - 2) / 3, (2 - 1) / 2], rtol=0, atol=1e-10)
+    gs = metrics.mode_gaps(a, (3, 2, 2), [f[0][:, :3], f[1][:, :2], f[2][:, :2]], sequential=True)
+    np.testing.assert_allclose(gs, [(3 - 2) / 3, (4 - 3) / 4, 1.0], rtol=0, atol=1e-6)
+
+
 # -------------------------------------------------------------- Algorithm 1
 def _tensor_b(n, v, seed):
     """Tensor B of PAPER.md:806-815 at desk scale: tendiag(v) x_k A_k."""
@@ -476,24 +522,3 @@ def test_a2_rank_above_unfolding_columns():
     for k, u in enumerate(res.factors):
         g = tucker.mode_product(g, u.T, k)
     np.testing.assert_allclose(res.core, g, atol=1e-10)
-
-
-def test_flip_hook_is_a_pure_sign_change():
-    """The parity harness's C6 near-tie hook: flip={} equals no flip; flipping a column of the
-    last mode's U_d negates that column and the matching core slice and nothing else (no later
-    mode sees it), so the Tucker approximation and its RE are unchanged."""
-    rng = np.random.default_rng(11)
-    dims, ranks = (12, 10, 9), (3, 4, 2)
-    core = rng.standard_normal((5, 5, 4))
-    a = tucker_tensor(core, [orthonormal_factor(n, 5 if n > 9 else 4, rng) for n in dims], noise=1e-2, rng=rng)
-    base = tucker.rsthosvd(a, ranks, 2, 2, 3)
-    same = tucker.rsthosvd(a, ranks, 2, 2, 3, flip={})
-    for u, v in zip(base.factors, same.factors):
-        assert np.array_equal(u, v)
-    fl = tucker.rsthosvd(a, ranks, 2, 2, 3, flip={2: [1]})
-    assert np.array_equal(fl.factors[0], base.factors[0]) and np.array_equal(fl.factors[1], base.factors[1])
-    assert np.array_equal(fl.factors[2][:, 1], -base.factors[2][:, 1])
-    assert np.array_equal(fl.factors[2][:, 0], base.factors[2][:, 0])
-    assert np.allclose(fl.core[:, :, 1], -base.core[:, :, 1], rtol=0, atol=1e-12)
-    assert np.allclose(fl.core[:, :, 0], base.core[:, :, 0], rtol=0, atol=1e-12)
-    assert abs(metrics.relative_error(a, fl.core, fl.factors) - metrics.relative_error(a, base.core, base.factors)) < 1e-12
