@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librtucker.so")
-SOURCES = ["rtk_tile.cu", "rtk_small.cu", "rtk_solve.cu", "rtk_tc.cu", "rtk_fused.cu", "rtk_omega.cu", "rtk_api.cu"]
+SOURCES = ["rtk_tile.cu", "rtk_small.cu", "rtk_solve.cu", "rtk_tc.cu", "rtk_fused.cu", "rtk_fused2.cu", "rtk_omega.cu", "rtk_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
          "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,764 @@
+// rtk_fused2.cu -- the fused single-HBM-pass 3xTF32 power step (Alg. 3/4 line 7, PAPER.md:261 /
+// :304, Y = M (M^T Q)) on a CTA PAIR (tcgen05 cta_group::2, M = 256 across two SMs of a TPC).
+//
+// Why a pair.  Per 32-K stage (128 x 64 x 32, three tf32 products = 384 tensor cycles) the
+// one-CTA engine (rtk_fused.cu) moves ~66 KB through each SM's shared memory: the streamed tile
+// in (TMA) and out (producers), 24 KB of B operand read by the 12 MMAs and 16 KB of Q planes per
+// op1 stage.  At 128 B/clk that is ~516 cycles -- more than the tensor work -- and the MMAs ran
+// at ~58 instead of 32 cycles each (ncu: tensor pipe 52 % active).  With cta_group::2 each SM
+// supplies only half of B (N/2 rows): 12 KB of B reads and 8 KB of Q per stage, ~385 cycles.
+//
+// Work split.  Pair-block J = 256 consecutive columns of the column-major unfolding M (n x m),
+// CTA r owning columns [128 r, 128 r + 128) of it.
+//   op1  W_J = M_J^T Q : M = 256 columns (CTA r's 128 as its TMEM lanes), K = all n rows
+//        (32 per stage), N = l padded; B = Q's hi/lo planes, CTA r holding N-half r.
+//        Every CTA ends with W for ITS 128 columns and all N -- no partial sums to exchange.
+//   op2  Y += M_J W_J  : M = 256 rows per pair-tile (CTA r's 128 as its lanes), K = the 256
+//        columns of J, N; B = W_J's hi/lo planes, CTA r holding N-half r: its own columns'
+//        half r plus the peer's columns' half r, which the peer sends through DSMEM (16 KB).
+// M_J is read from HBM by op1 and re-read (L2) by op2 one block later, as in the one-CTA engine.
+// The streamed operand reaches the tensor core through TMEM: producer warps split x = hi + lo
+// (hi = what the tf32 datapath reads, lo = x - trunc_tf32(x), exact) and tcgen05.st both planes;
+// 3 MMAs per K-step (A_lo B_hi + A_hi B_lo + A_hi B_hi, fp32 accumulate in TMEM).
+// Only the even CTA (the leader) issues MMAs; barriers that the MMA warp waits on live in the
+// leader (the peer arrives remotely), MMA completion is multicast to both CTAs' barriers.
+//
+// Warp roles (480 threads per CTA): 0 TMA A tiles, 1 MMA issuer (leader) + TMEM owner,
+// 2-9 producers (two groups alternating stages, one warp per TMEM lane quadrant), 10-13 epilogue
+// (W -> exchange -> op2 B planes; final Y), 14 TMA Q half-planes.
+// Y partials go to Ypart[pair][c][row] (row pitch nt * 256) for the fixed-order fp64 reduction.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "rtk_internal.h"
+#include "rtk_sm100.cuh"
+
+namespace rtk {
+using namespace sm100;
+
+namespace {
+
+constexpr int kPThreads = 480;
+constexpr int kPKS = 32;        // K per stage (4 MMA K-steps of 8)
+constexpr int kPRA = 6;         // A tile ring slots (16 KB each)
+constexpr int kPRQ = 6;         // Q half-plane ring slots
+constexpr int kPTile = 128 * 32 * 4;
+constexpr int kPBJ = 256;       // columns per pair-block
+constexpr int kPK2 = kPBJ / kPKS;   // op2 stages per pair-tile (8)
+
+// Role timers (-DRTK_PAIR_PROF=1 builds only; clock reads cost issue slots): summed wait / busy
+// cycles of the two CTAs of pair 0, printed by the host at the next launch.
+#ifndef RTK_PAIR_PROF
+#define RTK_PAIR_PROF 0
+#endif
+#if RTK_PAIR_PROF
+__device__ unsigned long long g_pair_prof[2][32];
+#define PCLK() clock64()
+#define PACC(slot, t0)                                                                                  \
+  do {                                                                                                  \
+    const int _w = threadIdx.x >> 5;                                                                    \
+    if (blockIdx.x < 2 && (threadIdx.x & 31) == 0 && ((slot) < 8 || (slot) >= 16 || _w == 2) &&         \
+        ((slot) < 20 || (slot) > 23 || _w == 10))                                                       \
+      atomicAdd(&g_pair_prof[blockIdx.x][slot], (unsigned long long)(clock64() - (t0)));                \
+  } while (0)
+#else
+#define PCLK() 0LL
+#define PACC(slot, t0) do { (void)(t0); } while (0)
+#endif
+
+struct PairArgs {
+  int n;
+  int64_t m;
+  int nt;          // pair row tiles (256 rows each), <= 4
+  int nk1;         // op1 stages per pair-block: ceil(n / 32)
+  int64_t nblk;    // pair-blocks: ceil(m / 256)
+  float* Ypart;    // [P][N][nt * 256]
+  const int* stop; // Alg. B.1 stop flag (nullptr: none)
+  int dbg;         // ablations (RTK_PAIR_DBG, timing only, results wrong): 1 no MMAs, 2 no A loads,
+                   // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads
+};
+
+__device__ __forceinline__ uint32_t p_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void p_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t p_mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier anywhere in the cluster (own CTA included), release at cluster scope:
+// orders this thread's prior shared-memory writes / reads before the peer's acquire (per-block
+// exchange handshakes only -- it costs a MEMBAR.GPU)
+__device__ __forceinline__ void p_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// per-stage signal (default .release.cta semantics, no GPU-scope membar): the TMEM stores it
+// publishes are ordered by tcgen05.wait::st + tcgen05.fence::before_thread_sync
+__device__ __forceinline__ void p_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void p_wait_cluster(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE%=;\nbra.uni LAB_WAIT%=;\nDONE%=:\n}\n" ::"r"(smem_addr(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void p_wait_sleep(uint64_t* b, uint32_t phase) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(phase)
+        : "memory");
+    if (ok) break;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void p_st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+// local TMA load (own barrier) with an L2 cache policy
+__device__ __forceinline__ void p_tma_load(void* dst, const CUtensorMap* m, int x, int y, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], "
+      "%5;" ::"r"(smem_addr(dst)),
+      "l"((uint64_t)m), "r"(x), "r"(y), "r"(smem_addr(b)), "l"(pol)
+      : "memory");
+}
+// pair TMA load: data into this CTA's shared memory, completion signalled on the barrier at
+// cluster address `cbar` (the leader's), .cta_group::2
+__device__ __forceinline__ void p_tma_load_pair(void* dst, const CUtensorMap* m, int x, int y, uint32_t cbar,
+                                                uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+      "l"((uint64_t)m), "r"(x), "r"(y), "r"(cbar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t p_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t p_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Issue recipe (measured, scripts/micro/mma_stream.cu + the SASS): the MMA warp branches on
+// elect.sync at the C++ level and the tcgen05 asm carries no predicate of its own; with the TMEM
+// base a literal (a 512-column allocation starts at column 0) and the descriptors built from
+// the shared-memory base and uniform loop counters, ptxas keeps every operand in uniform
+// registers and emits back-to-back UTCHMMA.  With the elect inside each asm block every MMA paid
+// ~5 R2UR conversions on the elected lane (~53 cycles per MMA against the 32-cycle tensor floor).
+__device__ __forceinline__ uint32_t p_elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, 0xffffffff;\n@px mov.s32 %0, 1;\n}\n"
+               : "+r"(pred));
+  return pred;
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void p_mma3(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t bhi, uint64_t blo,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %6, p;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], [%1], %4, %6, 1;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], [%1], %3, %6, 1;\n}\n" ::"r"(d),
+      "r"(ahi), "r"(alo), "l"(bhi), "l"(blo), "r"(acc), "n"(IDESC));
+}
+__device__ __forceinline__ void p_commit_one(uint64_t* b) {   // elected lane only
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(b)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// the three 3xTF32 products of one K-step on the pair: D (+)= A_lo B_hi + A_hi B_lo + A_hi B_hi
+template <uint32_t IDESC>
+__device__ __forceinline__ void p_umma3(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t bhi, uint64_t blo,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %5, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %6, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], [%1], %4, %6, 1;\n"
+      "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], [%1], %3, %6, 1;\n}\n" ::"r"(d),
+      "r"(ahi), "r"(alo), "l"(bhi), "l"(blo), "r"(acc), "n"(IDESC));
+}
+// arrive (once) on the same-offset mbarrier of both CTAs when this thread's MMAs complete
+__device__ __forceinline__ void p_commit_mc(uint64_t* b) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_addr(b)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void bar_wait_addr(uint32_t addr, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE%=;\nbra.uni LAB_WAIT%=;\nDONE%=:\n}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bar_arrive_addr(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void p_tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+}  // namespace
+
+// SA: TMEM A stages (2: W double-buffered; 3: W single-buffered -- safe with this stage order,
+// where op1(jb+1) follows op2(jb-1), long after W(jb) was drained -- and one more stage in flight)
+template <int N, int SA>
+__global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                                  const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmA2,
+                                                                  const PairArgs a) {
+  constexpr int N2 = N / 2;                  // B rows held by each CTA
+  constexpr int QS = 2 * N2 * 128;           // Q ring slot: hi | lo half-planes of 32 rows
+  constexpr int PL = (kPBJ / 32) * N2 * 128; // one op2 B plane: 256 columns x N2
+  constexpr uint32_t IDESC = idesc_tf32(256, N, 0, 0);
+  constexpr int NW = SA == 2 ? 2 : 1;         // W buffers
+  constexpr int TA0 = 256 + NW * N;          // TMEM: Y tiles at 0, W buffers at 256, A ring
+  static_assert(N % 16 == 0 && N >= 16 && N <= 64, "cta_group::2 N");
+  static_assert(TA0 + 2 * kPKS * SA <= 512, "TMEM budget");
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = smraw + ((1024u - (smem_addr(smraw) & 1023u)) & 1023u);
+  uint8_t* smR = sm;                          // kPRA x kPTile
+  uint8_t* smQ = smR + kPRA * kPTile;         // kPRQ x QS
+  uint8_t* smP = smQ + kPRQ * QS;             // hi plane | lo plane
+  float* rbuf = (float*)(smP + 2 * PL);       // 128 x N2 received from the peer
+  __shared__ __align__(8) uint64_t r_full[kPRA], r_empty[kPRA], q_full[kPRQ], q_empty[kPRQ];
+  __shared__ __align__(8) uint64_t a_full[SA], a_empty[SA], w_full[2], w_empty[2];
+  __shared__ __align__(8) uint64_t p_full, p_empty, y_full, x_full, credit;
+  __shared__ uint32_t tbase_s;
+
+  pdl_wait();
+  if (a.stop && *(volatile const int*)a.stop) return;   // uniform over the grid: before any barrier
+  const int dbg = RTK_PAIR_PROF ? a.dbg : 0;          // ablations exist only in profiling builds
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = p_cluster_rank(), peer = rank ^ 1u;
+  const bool leader = rank == 0;
+  const int64_t pid = blockIdx.x >> 1, P = gridDim.x >> 1;
+  const int64_t nb = (a.nblk > pid) ? (a.nblk - pid + P - 1) / P : 0;   // pair-blocks of this pair
+  const int nk1 = a.nk1, nk2 = a.nt * kPK2;
+  const int64_t total = nb * (nk1 + nk2);
+
+  // stage walk shared by the TMA, MMA and producer warps:
+  //   op1(0), [op1(1)], op2(0), op1(2), op2(1), ..., op2(nb-1)
+  struct It { int op; int64_t jb; int k; };
+  auto adv = [&](It& t) {
+    ++t.k;
+    if (t.op == 1 && t.k == nk1) {
+      t.k = 0;
+      if (t.jb == 0 && nb > 1) { t.jb = 1; }
+      else { t.op = 2; t.jb = t.jb - (t.jb == 0 ? 0 : 1); }
+    } else if (t.op == 2 && t.k == nk2) {
+      t.k = 0;
+      if (t.jb + 2 < nb) { t.op = 1; t.jb += 2; }
+      else { t.jb += 1; }
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPRA; ++s) { bar_init(&r_full[s], 1); bar_init(&r_empty[s], 4); }
+    for (int s = 0; s < kPRQ; ++s) { bar_init(&q_full[s], 1); bar_init(&q_empty[s], 1); }
+    for (int s = 0; s < SA; ++s) { bar_init(&a_full[s], 8); bar_init(&a_empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { bar_init(&w_full[b], 1); bar_init(&w_empty[b], 8); }
+    bar_init(&p_full, 8); bar_init(&p_empty, 1); bar_init(&y_full, 1);
+    bar_init(&x_full, 1); bar_init(&credit, 4);
+    bar_fence_init();
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmA2);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  p_cluster_sync();   // both CTAs' barriers initialised and TMEM allocated before any cross-CTA use
+  tc_fence_after();
+  // a 512-column allocation owns the whole TMEM: its base is column 0 of lane 0 (the literal keeps
+  // the MMA operands uniform, see p_elect_one)
+  if (tbase_s != 0u) __trap();
+  constexpr uint32_t tbase = 0u;
+  auto colbase = [&](int64_t jb) -> int64_t { return (pid + jb * P) * kPBJ; };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA: A tiles (own ring)
+    if (lane == 0) {
+      It t = {1, 0, 0};
+      const uint64_t pol_keep = p_policy_last(), pol_drop = p_policy_first();
+      int sl = 0;
+      uint32_t ph = 0;
+      for (int64_t s = 0; s < total; ++s) {
+        { const long long _t0 = PCLK(); bar_wait(&r_empty[sl], ph ^ 1); PACC(17, _t0); }
+        uint8_t* dst = smR + sl * kPTile;
+        const int64_t c0 = colbase(t.jb);
+        if (dbg & 2) {
+          bar_arrive(&r_full[sl]);
+        } else if (t.op == 1) {
+          bar_expect_tx(&r_full[sl], kPTile);   // [128 columns j][32 rows i], SW128: rows 32k.., this CTA's 128 columns
+          p_tma_load(dst, &tmA, kPKS * t.k, (int)(c0 + 128 * rank), &r_full[sl], pol_keep);
+        } else {           // [32 columns][128 rows]: pair-tile t.k / 8, this CTA's 128 rows
+          bar_expect_tx(&r_full[sl], kPTile);
+          const int tt = t.k / kPK2, kq = t.k % kPK2;
+          p_tma_load(dst, &tmA2, 256 * tt + 128 * (int)rank, (int)(c0 + kPKS * kq), &r_full[sl], pol_drop);
+        }
+        if (++sl == kPRA) { sl = 0; ph ^= 1; }
+        adv(t);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader)
+    if (leader) {
+      const uint64_t q0 = sdesc_sw128(smem_addr(smQ), 16, 1024);
+      const uint64_t p0 = sdesc_sw128(smem_addr(smP), 16, 1024);
+      const bool mma_on = !(dbg & 1);
+      int sa = 0;            // TMEM A stage of the current stage (counter, no division)
+      uint32_t aph = 0;      // its phase
+      int qsl = 0;
+      uint32_t qph = 0;
+      auto next_a = [&]() { if (++sa == SA) { sa = 0; aph ^= 1; } };
+      const long long _tm0 = PCLK();
+      for (int64_t jb = 0; jb <= nb; ++jb) {
+        if (jb < nb) {   // op1(jb) -> W buffer jb % NW
+          const int b = NW == 2 ? (int)(jb & 1) : 0;
+          const int64_t wu = NW == 2 ? (jb >> 1) : jb;   // use count of buffer b
+          { const long long _t0 = PCLK(); p_wait_cluster(&w_empty[b], (uint32_t)((wu & 1) ^ 1)); PACC(5, _t0); }
+          tc_fence_after();
+          const uint32_t d = 256u + (uint32_t)(b * N);
+          for (int kc = 0; kc < nk1; ++kc) {
+            { const long long _t0 = PCLK(); bar_wait(&q_full[qsl], qph); PACC(2, _t0); }
+            { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(1, _t0); }
+            tc_fence_after();
+            if (p_elect_one()) {
+              const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
+              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+              if (mma_on) {
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8)
+                  p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+                                qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (kc | k8) != 0);
+              }
+              p_commit_one(&a_empty[sa]);
+              p_commit_one(&q_empty[qsl]);
+            }
+            __syncwarp();
+            next_a();
+            if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
+          }
+          if (p_elect_one()) p_commit_one(&w_full[b]);
+          __syncwarp();
+        }
+        const int64_t j2 = jb - 1;
+        if (j2 >= 0 && j2 < nb) {   // op2(j2)
+          { const long long _t0 = PCLK(); p_wait_cluster(&p_full, (uint32_t)(j2 & 1)); PACC(4, _t0); }
+          tc_fence_after();
+          for (int t = 0; t < a.nt; ++t) {
+            const uint32_t d = (uint32_t)(t * N);
+#pragma unroll 1
+            for (int kq = 0; kq < kPK2; ++kq) {
+              { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
+              tc_fence_after();
+              if (p_elect_one()) {
+                const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+                if (mma_on) {
+#pragma unroll
+                  for (int k8 = 0; k8 < 4; ++k8) {
+                    const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
+                    p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
+                                  p0 + (uint64_t)((PL + boff) >> 4), (j2 > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
+                  }
+                }
+                p_commit_one(&a_empty[sa]);
+              }
+              __syncwarp();
+              next_a();
+            }
+          }
+          if (p_elect_one()) p_commit_one(&p_empty);
+          __syncwarp();
+        }
+      }
+      if (p_elect_one()) p_commit_one(&y_full);
+      __syncwarp();
+      if (lane == 0) PACC(0, _tm0);
+    }
+  } else if (warp < 10) {
+    // ---------------------------------------------------------------- producers: tile -> split -> TMEM
+    // Instruction-lean loop (the producers' issue slots bound the stage rate): ring slot / TMEM
+    // stage / phases are running counters, the stage walk is a segment counter (a producer needs
+    // only the op of a stage), lo = x - trunc_tf32(x) in packed FADD2.
+    const int q = warp & 3, g = (warp - 2) >> 2;
+    const int lt = 32 * q + lane;   // TMEM lane = op1 column / op2 row within this CTA's 128
+    const uint32_t tq0 = tbase + ((uint32_t)(32 * q) << 16) + TA0;
+    const uint32_t afull_c0 = p_mapa(smem_addr(&a_full[0]), 0);   // the leader's barriers
+    const uint32_t rfull0 = smem_addr(&r_full[0]), rempty0 = smem_addr(&r_empty[0]), aempty0 = smem_addr(&a_empty[0]);
+    const uint32_t tile1 = smem_addr(smR) + (uint32_t)lt * 128u;   // op1: row lt of the SW128 tile
+    const uint32_t tile2 = smem_addr(smR) + (uint32_t)lt * 4u;     // op2: column lt of [32 c][128 i]
+    const uint32_t sw = (uint32_t)(lt & 7);
+    // segments: op1 x nk1 [block 0], (op1 x nk1 [block 1]), then (op2 x nk2, op1 x nk1)..., op2 x nk2 ...
+    int op = 1, rem = nk1;                        // op of the current stage and stages left in its segment
+    int64_t seg_blk = 0;                           // block of the current segment
+    auto step = [&]() {
+      if (--rem > 0) return;
+      if (op == 1) {
+        if (seg_blk == 0 && nb > 1) { seg_blk = 1; rem = nk1; }
+        else { op = 2; seg_blk = seg_blk == 0 ? 0 : seg_blk - 1; rem = nk2; }
+      } else {
+        if (seg_blk + 2 < nb) { op = 1; seg_blk += 2; rem = nk1; }
+        else { seg_blk += 1; rem = nk2; }
+      }
+    };
+    if (g == 1) step();
+    int sl = g, ts = g;                            // ring slot / TMEM stage of this group's stage
+    uint32_t rph = 0, tph = 0;
+    const long long _tp0 = PCLK();
+    for (int64_t s = g; s < total; s += 2) {
+      { const long long _t0 = PCLK(); bar_wait_addr(rfull0 + 8u * (uint32_t)sl, rph); PACC(9, _t0); }
+      float v[kPKS];
+#if RTK_PAIR_PROF
+      if (dbg & 4) {
+#pragma unroll
+        for (int c = 0; c < kPKS; ++c) v[c] = (float)(c + lt);
+      } else
+#endif
+      if (op == 1) {
+        const uint32_t base = tile1 + (uint32_t)sl * kPTile;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = lds128(base + ((((uint32_t)c) ^ sw) << 4));
+          v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
+        }
+      } else {
+        const uint32_t base = tile2 + (uint32_t)sl * kPTile;
+#pragma unroll
+        for (int c = 0; c < kPKS; ++c) v[c] = lds32(base + (uint32_t)(c * 512));
+      }
+      float lo[kPKS];
+#pragma unroll
+      for (int e = 0; e < kPKS; e += 2) {
+        const float2 d = __fadd2_rn(make_float2(v[e], v[e + 1]), make_float2(-tf32_trunc(v[e]), -tf32_trunc(v[e + 1])));
+        lo[e] = d.x; lo[e + 1] = d.y;
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive_addr(rempty0 + 8u * (uint32_t)sl);
+      { const long long _t0 = PCLK(); bar_wait_addr(aempty0 + 8u * (uint32_t)ts, tph ^ 1u); PACC(10, _t0); }
+      tc_fence_after();
+      const uint32_t tq = tq0 + (uint32_t)(2 * kPKS * ts);
+#if RTK_PAIR_PROF
+      if (!(dbg & 8))
+#endif
+      {
+        p_tmem_st32(tq, v);
+        p_tmem_st32(tq + kPKS, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) p_arrive_remote(afull_c0 + 8u * (uint32_t)ts);
+      sl += 2;
+      if (sl >= kPRA) { sl -= kPRA; rph ^= 1u; }
+      ts += 2;
+      if (ts >= SA) { ts -= SA; tph ^= 1u; }
+      step();
+      step();
+    }
+    PACC(8, _tp0);
+  } else if (warp < 14) {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int j = 32 * q + lane;   // this CTA's block column = TMEM lane of W
+    const uint32_t wempty_c[2] = {p_mapa(smem_addr(&w_empty[0]), 0), p_mapa(smem_addr(&w_empty[1]), 0)};
+    const uint32_t pfull_c = p_mapa(smem_addr(&p_full), 0);
+    const uint32_t rdst = p_mapa(smem_addr(rbuf + j * N2), peer);
+    const uint32_t rbar = p_mapa(smem_addr(&x_full), peer);
+    const uint32_t rcredit = p_mapa(smem_addr(&credit), peer);
+    const long long _te0 = PCLK();
+    for (int64_t jb = 0; jb < nb; ++jb) {
+      const int b = NW == 2 ? (int)(jb & 1) : 0;
+      { const long long _t0 = PCLK(); p_wait_sleep(&w_full[b], (uint32_t)((NW == 2 ? (jb >> 1) : jb) & 1)); PACC(21, _t0); }
+      tc_fence_after();
+      float w[N];
+#pragma unroll
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + 256 + b * N + c0, v);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) w[c0 + c] = v[c];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) p_arrive_cluster(wempty_c[b]);
+      // exchange: the peer's N-half of my column j goes to the peer's rbuf row j; I receive the
+      // peer's column j, my N-half.  Row j's 16-B chunk c4 sits at (c4 + j) mod N2/4 so that the
+      // reads below are bank-conflict-free.
+      const uint32_t px = (uint32_t)(jb & 1);
+      if (threadIdx.x == 10 * 32)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&x_full)),
+                     "r"((uint32_t)(128 * N2 * 4))
+                     : "memory");
+      // own N-half / the peer's N-half of my column (selects keep the register indices static)
+      float wo[N2], wsnd[N2];
+#pragma unroll
+      for (int c = 0; c < N2; ++c) {
+        wo[c] = rank ? w[N2 + c] : w[c];
+        wsnd[c] = rank ? w[c] : w[N2 + c];
+      }
+      { const long long _t0 = PCLK(); p_wait_cluster(&credit, px ^ 1); PACC(22, _t0); }   // the peer has read my previous send
+#pragma unroll
+      for (int c4 = 0; c4 < N2 / 4; ++c4)
+        p_st_async_v4(rdst + 16 * ((c4 + j) % (N2 / 4)),
+                      make_float4(wsnd[4 * c4], wsnd[4 * c4 + 1], wsnd[4 * c4 + 2], wsnd[4 * c4 + 3]), rbar);
+      { const long long _t0 = PCLK(); p_wait_cluster(&x_full, px); PACC(22, _t0); }
+      float pw[N2];
+#pragma unroll
+      for (int c4 = 0; c4 < N2 / 4; ++c4) {
+        const float4 x = *reinterpret_cast<const float4*>(rbuf + j * N2 + 4 * ((c4 + j) % (N2 / 4)));
+        pw[4 * c4] = x.x; pw[4 * c4 + 1] = x.y; pw[4 * c4 + 2] = x.z; pw[4 * c4 + 3] = x.w;
+      }
+      __syncwarp();
+      if (lane == 0) p_arrive_cluster(rcredit);
+      // op2 B planes of this CTA (N-half `rank`): own column at K index 128 rank + j, the peer's
+      // column at 128 peer + j; hi = rna tf32, lo exact; once op2(jb-1) has released the planes
+      { const long long _t0 = PCLK(); p_wait_sleep(&p_empty, (uint32_t)((jb & 1) ^ 1)); PACC(23, _t0); }
+      const int ko = 128 * (int)rank + j, kp = 128 * (int)peer + j;
+#pragma unroll
+      for (int c = 0; c < N2; ++c) {
+        const float xo = wo[c], xp = pw[c];
+        const float ho = tf32_rna(xo), hp = tf32_rna(xp);
+        const uint32_t oo = (uint32_t)((ko >> 5) * (N2 * 128)) + sw128_offset(c, ko & 31);
+        const uint32_t op = (uint32_t)((kp >> 5) * (N2 * 128)) + sw128_offset(c, kp & 31);
+        *reinterpret_cast<float*>(smP + oo) = ho;
+        *reinterpret_cast<float*>(smP + PL + oo) = xo - ho;
+        *reinterpret_cast<float*>(smP + op) = hp;
+        *reinterpret_cast<float*>(smP + PL + op) = xp - hp;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) p_arrive_cluster(pfull_c);
+    }
+    PACC(20, _te0);
+    // ---- final: this CTA's Y rows (its half of every pair-tile) -> Ypart[pair][c][row]
+    const int rows_tot = a.nt * 256;
+    float* yp = a.Ypart + pid * (int64_t)N * rows_tot;
+    if (nb > 0) {
+      p_wait_sleep(&y_full, 0);
+      tc_fence_after();
+    }
+    for (int t = 0; t < a.nt; ++t) {
+      const int i = 256 * t + 128 * (int)rank + j;
+#pragma unroll
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        if (nb > 0) tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + t * N + c0, v);
+        else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) v[c] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) yp[(int64_t)(c0 + c) * rows_tot + i] = v[c];
+      }
+    }
+    tc_fence_before();
+  } else if (lane == 0) {
+    // ---------------------------------------------------------------- TMA: Q half-planes (pair)
+    // op1 stage k of every block: rows 32k.., N-half `rank` of the hi and lo planes, completion on
+    // the leader's q_full (which expects both halves)
+    const uint64_t pol_keep = p_policy_last();
+    const uint32_t qfull0 = p_mapa(smem_addr(&q_full[0]), 0);
+    int sl = 0;
+    uint32_t ph = 0;
+    for (int64_t jb = 0; jb < nb; ++jb)
+      for (int k = 0; k < nk1; ++k) {
+        { const long long _t0 = PCLK(); bar_wait(&q_empty[sl], ph ^ 1); PACC(24, _t0); }
+        uint8_t* sq = smQ + sl * QS;
+        const uint32_t cb = qfull0 + 8u * (uint32_t)sl;
+        if (dbg & 16) {
+          if (leader) bar_arrive(&q_full[sl]);
+        } else {
+          if (leader) bar_expect_tx(&q_full[sl], 2 * QS);   // both CTAs' halves
+          p_tma_load_pair(sq, &tmQ, kPKS * k, (int)rank * N2, cb, pol_keep);
+          p_tma_load_pair(sq + N2 * 128, &tmQ, kPKS * k, N + (int)rank * N2, cb, pol_keep);
+        }
+        if (++sl == kPRQ) { sl = 0; ph ^= 1; }
+      }
+  }
+  __syncthreads();
+  p_cluster_sync();   // no CTA releases TMEM / leaves while the peer may still use it
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+// ---------------------------------------------------------------------- host side
+typedef CUresult (*PFN_encode2_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encode2_t pair_encode_fn() {
+  static PFN_encode2_t fn = nullptr;
+  static bool done = false;
+  if (!done) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_encode2_t)p;
+    done = true;
+  }
+  return fn;
+}
+
+bool pair_supported(const View& v, int l) {
+  const char* e = getenv("RTK_PAIR");
+  if (e && e[0] == '0') return false;
+  const int N = tc_npad(l);
+  if (!N) return false;
+  if (!(v.P == 1 && v.si == 1 && v.ss >= v.n && v.ss % 4 == 0 && ((uintptr_t)v.base % 16) == 0)) return false;
+  if (v.n > 1024) return false;
+  return pair_encode_fn() != nullptr;
+}
+
+size_t pair_ypart_floats(const View& v, int l, int grid) {
+  const int N = tc_npad(l), nt = (v.n + 255) / 256;
+  return (size_t)(grid / 2) * N * nt * 256;
+}
+
+template <int N, int SA>
+static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, const CUtensorMap& ta2, const PairArgs& a,
+                               int grid, cudaStream_t st) {
+  const size_t smem = 1024 + (size_t)kPRA * kPTile + (size_t)kPRQ * 2 * (N / 2) * 128 +
+                      2 * (size_t)(kPBJ / 32) * (N / 2) * 128 + (size_t)128 * (N / 2) * 4;
+  cudaError_t e = cudaFuncSetAttribute(pair_power_kernel<N, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kPThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, pair_power_kernel<N, SA>, tq, ta, ta2, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// One power step Y = M M^T Q on the pair engine from Q's hi/lo planes [2N][pld].
+// Ypart[grid/2][N][nt*256]; returns the partial count and row pitch.
+cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
+                       int* rows_out, cudaStream_t st, const int* stop) {
+  const int N = tc_npad(l), nt = (v.n + 255) / 256;
+  const int64_t m = v.m();
+  const int64_t nblk = (m + kPBJ - 1) / kPBJ;
+  int pairs = std::max(1, grid / 2);
+  pairs = (int)std::min<int64_t>(pairs, std::max<int64_t>(1, nblk));   // no idle pairs (zero partials)
+  PairArgs a;
+  a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + kPKS - 1) / kPKS; a.nblk = nblk;
+  a.Ypart = Ypart; a.stop = stop;
+  a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
+  CUtensorMap tq, ta, ta2;
+  memset(&tq, 0, sizeof(tq));
+  memset(&ta, 0, sizeof(ta));
+  memset(&ta2, 0, sizeof(ta2));
+  const cuuint32_t es[2] = {1, 1};
+  {   // op1 A tiles: box {32 rows, 128 columns}, SWIZZLE_128B ([128 j][32 i])
+    cuuint64_t dims[2] = {(cuuint64_t)v.n, (cuuint64_t)m};
+    cuuint64_t strides[1] = {(cuuint64_t)v.ss * 4};
+    cuuint32_t box[2] = {32, 128};
+    if (pair_encode_fn()(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {   // op2 A tiles: box {128 rows, 32 columns}, no swizzle ([32 c][128 i])
+    cuuint64_t dims[2] = {(cuuint64_t)v.n, (cuuint64_t)m};
+    cuuint64_t strides[1] = {(cuuint64_t)v.ss * 4};
+    cuuint32_t box[2] = {128, 32};
+    if (pair_encode_fn()(&ta2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(v.base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {   // Q planes [2N][pld]: box {32 rows i, N/2 columns c}, SWIZZLE_128B ([N/2 c][32 i])
+    cuuint64_t dims[2] = {(cuuint64_t)v.n, (cuuint64_t)(2 * N)};
+    cuuint64_t strides[1] = {(cuuint64_t)pld * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)(N / 2)};
+    if (pair_encode_fn()(&tq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(planes), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  *G_out = pairs;
+  *rows_out = nt * 256;
+#if RTK_PAIR_PROF
+  {   // role timers of the previous launch (pair 0), then reset
+    static int calls = 0;
+    unsigned long long h[2][32];
+    if (calls++ > 0 && cudaMemcpyFromSymbol(h, g_pair_prof, sizeof(h)) == cudaSuccess)
+      for (int r = 0; r < 2; ++r)
+        fprintf(stderr,
+                "[pair prof cta%d] mma total %llu wait a_full(op1) %llu q_full %llu a_full(op2) %llu p_full %llu "
+                "w_empty %llu | prod total %llu r_full %llu a_empty %llu st %llu | tma r_empty %llu | epi total %llu "
+                "w_full %llu exch %llu p_empty %llu | q q_empty %llu\n",
+                r, h[r][0], h[r][1], h[r][2], h[r][3], h[r][4], h[r][5], h[r][8], h[r][9], h[r][10], h[r][11], h[r][17],
+                h[r][20], h[r][21], h[r][22], h[r][23], h[r][24]);
+    unsigned long long z[2][32] = {};
+    cudaMemcpyToSymbol(g_pair_prof, z, sizeof(z));
+  }
+#endif
+  const char* se = getenv("RTK_PAIR_SA");
+  const bool sa3 = !(se && se[0] == '2');
+  switch (N) {
+    case 16: return sa3 ? pair_launch<16, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<16, 2>(tq, ta, ta2, a, 2 * pairs, st);
+    case 32: return sa3 ? pair_launch<32, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<32, 2>(tq, ta, ta2, a, 2 * pairs, st);
+    case 48: return sa3 ? pair_launch<48, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<48, 2>(tq, ta, ta2, a, 2 * pairs, st);
+    default: return sa3 ? pair_launch<64, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<64, 2>(tq, ta, ta2, a, 2 * pairs, st);
+  }
+}
+
+}  // namespace rtk

@@ -128,6 +128,12 @@ cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool
                         float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1,
                         const int* stop = nullptr, const float* om = nullptr);
 
+// ---- fused power step on a CTA pair, tcgen05 cta_group::2 (rtk_fused2.cu) ---------------
+bool pair_supported(const View& v, int l);
+size_t pair_ypart_floats(const View& v, int l, int grid);
+cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
+                       int* rows_out, cudaStream_t st, const int* stop);
+
 // ---- Appendix D sketch types (rtk_omega.cu) ------------------------------------------
 // Materialise Omega_k rows [row0, row0 + rows) x l (row-major [j][l]) of the given type for the
 // mode-mode1 unfolding of a tensor with extents dims[0..d-1]; tabs: scratch for the Khatri-Rao

@@ -1,0 +1,4 @@
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "fused" 2>&1 | tail -2
+for i in 1 2; do timeout 60 python scripts/one_power_step.py 1000 1000000 60 20; done
+RTK_PAIR=0 timeout 60 python scripts/one_power_step.py 1000 1000000 60 20
+timeout 120 python scripts/prof_solve.py c5 3

@@ -41,8 +41,12 @@ def run_both(a, ranks, p, q, seed, sequential, shift=True):
 # (<= 1e-3) with EW_EPS = 1e-5 (fp32 rounding ~6e-8 per operation, grown over K-long sums and q+1
 # passes; 10x the measured worst case).  The core is compared element-wise against the fp64 mode
 # products of the GPU's OWN factors (A x_1 U_1^T ... x_d U_d^T), which checks the shrink / core
-# kernels entry by entry independently of how well the factors are determined.
+# kernels entry by entry independently of how well the factors are determined, with the
+# componentwise bound of a floating-point sum: |dG| <= CORE_EPS * (|A| x_1 |U_1|^T ... x_d |U_d|^T)
+# (each core entry is a K = prod(n) term sum; fp32 storage of the shrunk intermediates and the
+# 3xTF32 / fp32 accumulation give ~1e-6 of that bound measured on C3/C5, so 2e-5 leaves 10x).
 EW_EPS = 1e-5
+CORE_EPS = 2e-5
 
 
 def elementwise_checks(a, g_core, g_U, orc, min_cols=0):
@@ -62,12 +66,16 @@ def elementwise_checks(a, g_core, g_U, orc, min_cols=0):
             checked += 1
     assert checked >= min_cols, (checked, min_cols)
     ref = np.asarray(a, dtype=np.float64)
+    bound = np.abs(ref)
     for k, u in enumerate(g_U):
-        ref = tucker.mode_product(ref, u.astype(np.float64).T, k)
-    cerr = float(np.max(np.abs(g_core.astype(np.float64) - ref)))
-    assert cerr <= 1e-5 * float(np.max(np.abs(ref))), (cerr, float(np.max(np.abs(ref))))
-    print(f"elementwise: {checked} factor columns, worst err/tol {worst:.3f}, core max err "
-          f"{cerr / max(float(np.max(np.abs(ref))), 1e-300):.2e} of max|core|")
+        u64 = u.astype(np.float64)
+        ref = tucker.mode_product(ref, u64.T, k)
+        bound = tucker.mode_product(bound, np.abs(u64).T, k)
+    dg = np.abs(g_core.astype(np.float64) - ref)
+    ratio = float(np.max(dg / np.maximum(bound, 1e-300)))
+    assert ratio <= CORE_EPS, (ratio, float(np.max(dg)), float(np.max(np.abs(ref))))
+    print(f"elementwise: {checked} factor columns, worst err/tol {worst:.3f}, core |dG|/componentwise "
+          f"bound {ratio:.2e}, max|dG| {float(np.max(dg)) / max(float(np.max(np.abs(ref))), 1e-300):.2e} of max|core|")
     return checked
 
 
