@@ -78,8 +78,43 @@ struct PairArgs {
   int64_t nblk;    // pair-blocks: ceil(m / 256)
   float* Ypart;    // [P][N][nt * 256]
   const int* stop; // Alg. B.1 stop flag (nullptr: none)
+  int lag;         // op1-only stages at the start of each step (PWalk::L)
   int dbg;         // ablations (RTK_PAIR_DBG, timing only, results wrong): 1 no MMAs, 2 no A loads,
                    // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads
+};
+
+// Stage order shared by the TMA, MMA and producer warps.  Step 0 = op1(0); step b (1 <= b < nb)
+// = the first L stages of op1(b), then op2(b-1) and the rest of op1(b) alternating stage by stage,
+// then whichever is left; step nb = op2(nb-1).  op2(b) thus re-reads block b about one step after
+// op1(b) read it (the pair-blocks in flight, 74 x 1 MB per step, stay inside the 126 MB L2; with
+// op1(b+1) and op2(b) back to back the reuse distance was 1.5 steps and every op2 tile missed),
+// and the L op1-only stages cover the W exchange / op2-plane latency before op2(b-1) needs them.
+struct PWalk {
+  int nk1, nk2, L;
+  int64_t nb;
+  int64_t b = 0;
+  int pos = 0, len = 0;
+  __device__ void init(int nk1_, int nk2_, int L_, int64_t nb_) {
+    nk1 = nk1_; nk2 = nk2_; L = L_ < nk1_ ? L_ : nk1_; nb = nb_;
+    b = 0; pos = 0; len = nk1;
+  }
+  __device__ void cur(int& op, int64_t& blk, int& k) const {
+    if (b == 0) { op = 1; blk = 0; k = pos; return; }
+    if (b == nb) { op = 2; blk = nb - 1; k = pos; return; }
+    if (pos < L) { op = 1; blk = b; k = pos; return; }
+    const int r = pos - L, mi = (nk1 - L) < nk2 ? (nk1 - L) : nk2;
+    if (r < 2 * mi) {
+      if (r & 1) { op = 1; blk = b; k = L + (r >> 1); }
+      else { op = 2; blk = b - 1; k = r >> 1; }
+    } else if (nk1 - L > nk2) { op = 1; blk = b; k = L + mi + (r - 2 * mi); }
+    else { op = 2; blk = b - 1; k = mi + (r - 2 * mi); }
+  }
+  __device__ void next() {
+    if (++pos < len) return;
+    ++b;
+    pos = 0;
+    len = (b == nb) ? nk2 : nk1 + nk2;
+  }
 };
 
 __device__ __forceinline__ uint32_t p_cluster_rank() {
@@ -209,6 +244,18 @@ __device__ __forceinline__ void p_commit_mc(uint64_t* b) {
       "h"((uint16_t)3)
       : "memory");
 }
+// both barriers' phases complete; the two try_waits are in flight together (one ~90-cycle
+// latency instead of two)
+__device__ __forceinline__ void bar_wait2(uint64_t* b1, uint32_t ph1, uint64_t* b2, uint32_t ph2) {
+  asm volatile(
+      "{\n.reg .pred P1, P2;\nLAB_WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P2, [%2], %3;\n"
+      "and.pred P1, P1, P2;\n"
+      "@P1 bra.uni DONE%=;\nbra.uni LAB_WAIT%=;\nDONE%=:\n}\n" ::"r"(smem_addr(b1)),
+      "r"(ph1), "r"(smem_addr(b2)), "r"(ph2)
+      : "memory");
+}
 __device__ __forceinline__ void bar_wait_addr(uint32_t addr, uint32_t phase) {
   asm volatile(
       "{\n.reg .pred P1;\nLAB_WAIT%=:\n"
@@ -280,21 +327,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   const int nk1 = a.nk1, nk2 = a.nt * kPK2;
   const int64_t total = nb * (nk1 + nk2);
 
-  // stage walk shared by the TMA, MMA and producer warps:
-  //   op1(0), [op1(1)], op2(0), op1(2), op2(1), ..., op2(nb-1)
-  struct It { int op; int64_t jb; int k; };
-  auto adv = [&](It& t) {
-    ++t.k;
-    if (t.op == 1 && t.k == nk1) {
-      t.k = 0;
-      if (t.jb == 0 && nb > 1) { t.jb = 1; }
-      else { t.op = 2; t.jb = t.jb - (t.jb == 0 ? 0 : 1); }
-    } else if (t.op == 2 && t.k == nk2) {
-      t.k = 0;
-      if (t.jb + 2 < nb) { t.op = 1; t.jb += 2; }
-      else { t.jb += 1; }
-    }
-  };
+  // stage order (TMA, MMA and producer warps alike): op1(0), [op1(1)], op2(0), op1(2), op2(1), ..., op2(nb-1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPRA; ++s) { bar_init(&r_full[s], 1); bar_init(&r_empty[s], 4); }
@@ -324,27 +357,31 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA: A tiles (own ring)
+    // walks the same segment sequence as the MMA warp: op1(0), [op1(1)], op2(0), op1(2), op2(1), ...
     if (lane == 0) {
-      It t = {1, 0, 0};
       const uint64_t pol_keep = p_policy_last(), pol_drop = p_policy_first();
       int sl = 0;
       uint32_t ph = 0;
-      for (int64_t s = 0; s < total; ++s) {
+      auto load = [&](int op, int x, int64_t y) {
         { const long long _t0 = PCLK(); bar_wait(&r_empty[sl], ph ^ 1); PACC(17, _t0); }
         uint8_t* dst = smR + sl * kPTile;
-        const int64_t c0 = colbase(t.jb);
         if (dbg & 2) {
           bar_arrive(&r_full[sl]);
-        } else if (t.op == 1) {
-          bar_expect_tx(&r_full[sl], kPTile);   // [128 columns j][32 rows i], SW128: rows 32k.., this CTA's 128 columns
-          p_tma_load(dst, &tmA, kPKS * t.k, (int)(c0 + 128 * rank), &r_full[sl], pol_keep);
-        } else {           // [32 columns][128 rows]: pair-tile t.k / 8, this CTA's 128 rows
+        } else {
           bar_expect_tx(&r_full[sl], kPTile);
-          const int tt = t.k / kPK2, kq = t.k % kPK2;
-          p_tma_load(dst, &tmA2, 256 * tt + 128 * (int)rank, (int)(c0 + kPKS * kq), &r_full[sl], pol_drop);
+          if (op == 1) p_tma_load(dst, &tmA, x, (int)y, &r_full[sl], pol_keep);   // [128 j][32 i], SW128
+          else p_tma_load(dst, &tmA2, x, (int)y, &r_full[sl], pol_drop);         // [32 c][128 i]
         }
         if (++sl == kPRA) { sl = 0; ph ^= 1; }
-        adv(t);
+      };
+      PWalk w;
+      w.init(nk1, nk2, a.lag, nb);
+      for (int64_t st = 0; st < total; ++st, w.next()) {
+        int op, k;
+        int64_t blk;
+        w.cur(op, blk, k);
+        if (op == 1) load(1, kPKS * k, colbase(blk) + 128 * rank);   // all rows of this CTA's 128 columns
+        else load(2, 256 * (k / kPK2) + 128 * (int)rank, colbase(blk) + kPKS * (k % kPK2));
       }
     }
   } else if (warp == 1) {
@@ -359,65 +396,60 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       uint32_t qph = 0;
       auto next_a = [&]() { if (++sa == SA) { sa = 0; aph ^= 1; } };
       const long long _tm0 = PCLK();
-      for (int64_t jb = 0; jb <= nb; ++jb) {
-        if (jb < nb) {   // op1(jb) -> W buffer jb % NW
-          const int b = NW == 2 ? (int)(jb & 1) : 0;
-          const int64_t wu = NW == 2 ? (jb >> 1) : jb;   // use count of buffer b
-          { const long long _t0 = PCLK(); p_wait_cluster(&w_empty[b], (uint32_t)((wu & 1) ^ 1)); PACC(5, _t0); }
-          tc_fence_after();
-          const uint32_t d = 256u + (uint32_t)(b * N);
-          for (int kc = 0; kc < nk1; ++kc) {
-            { const long long _t0 = PCLK(); bar_wait(&q_full[qsl], qph); PACC(2, _t0); }
-            { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(1, _t0); }
-            tc_fence_after();
-            if (p_elect_one()) {
-              const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
-              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
-              if (mma_on) {
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8)
-                  p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
-                                qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (kc | k8) != 0);
-              }
-              p_commit_one(&a_empty[sa]);
-              p_commit_one(&q_empty[qsl]);
-            }
-            __syncwarp();
-            next_a();
-            if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
+      PWalk w;
+      w.init(nk1, nk2, a.lag, nb);
+      for (int64_t st = 0; st < total; ++st, w.next()) {
+        int op, k;
+        int64_t blk;
+        w.cur(op, blk, k);
+        if (op == 1) {   // op1(blk) stage k -> W buffer blk % NW
+          const int b = NW == 2 ? (int)(blk & 1) : 0;
+          if (k == 0) {
+            const int64_t wu = NW == 2 ? (blk >> 1) : blk;   // use count of buffer b
+            { const long long _t0 = PCLK(); p_wait_cluster(&w_empty[b], (uint32_t)((wu & 1) ^ 1)); PACC(5, _t0); }
           }
-          if (p_elect_one()) p_commit_one(&w_full[b]);
-          __syncwarp();
-        }
-        const int64_t j2 = jb - 1;
-        if (j2 >= 0 && j2 < nb) {   // op2(j2)
-          { const long long _t0 = PCLK(); p_wait_cluster(&p_full, (uint32_t)(j2 & 1)); PACC(4, _t0); }
+          { const long long _t0 = PCLK(); bar_wait2(&q_full[qsl], qph, &a_full[sa], aph); PACC(1, _t0); }
           tc_fence_after();
-          for (int t = 0; t < a.nt; ++t) {
+          if (p_elect_one()) {
+            const uint32_t d = 256u + (uint32_t)(b * N);
+            const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
+            const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+            if (mma_on) {
+#pragma unroll
+              for (int k8 = 0; k8 < 4; ++k8)
+                p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+                              qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (k | k8) != 0);
+            }
+            p_commit_one(&a_empty[sa]);
+            p_commit_one(&q_empty[qsl]);
+            if (k == nk1 - 1) p_commit_one(&w_full[b]);
+          }
+          __syncwarp();
+          if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
+        } else {         // op2(blk) stage k: pair-tile k / 8, K chunk k % 8
+          if (k == 0) {
+            { const long long _t0 = PCLK(); p_wait_cluster(&p_full, (uint32_t)(blk & 1)); PACC(4, _t0); }
+          }
+          { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
+          tc_fence_after();
+          if (p_elect_one()) {
+            const int t = k / kPK2, kq = k % kPK2;
             const uint32_t d = (uint32_t)(t * N);
-#pragma unroll 1
-            for (int kq = 0; kq < kPK2; ++kq) {
-              { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
-              tc_fence_after();
-              if (p_elect_one()) {
-                const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
-                if (mma_on) {
+            const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+            if (mma_on) {
 #pragma unroll
-                  for (int k8 = 0; k8 < 4; ++k8) {
-                    const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
-                    p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
-                                  p0 + (uint64_t)((PL + boff) >> 4), (j2 > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
-                  }
-                }
-                p_commit_one(&a_empty[sa]);
+              for (int k8 = 0; k8 < 4; ++k8) {
+                const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
+                p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
+                              p0 + (uint64_t)((PL + boff) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
               }
-              __syncwarp();
-              next_a();
             }
+            p_commit_one(&a_empty[sa]);
+            if (k == nk2 - 1) p_commit_one(&p_empty);
           }
-          if (p_elect_one()) p_commit_one(&p_empty);
           __syncwarp();
         }
+        next_a();
       }
       if (p_elect_one()) p_commit_one(&y_full);
       __syncwarp();
@@ -436,18 +468,14 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const uint32_t tile1 = smem_addr(smR) + (uint32_t)lt * 128u;   // op1: row lt of the SW128 tile
     const uint32_t tile2 = smem_addr(smR) + (uint32_t)lt * 4u;     // op2: column lt of [32 c][128 i]
     const uint32_t sw = (uint32_t)(lt & 7);
-    // segments: op1 x nk1 [block 0], (op1 x nk1 [block 1]), then (op2 x nk2, op1 x nk1)..., op2 x nk2 ...
-    int op = 1, rem = nk1;                        // op of the current stage and stages left in its segment
-    int64_t seg_blk = 0;                           // block of the current segment
+    PWalk w;
+    w.init(nk1, nk2, a.lag, nb);
+    int op = 1;
     auto step = [&]() {
-      if (--rem > 0) return;
-      if (op == 1) {
-        if (seg_blk == 0 && nb > 1) { seg_blk = 1; rem = nk1; }
-        else { op = 2; seg_blk = seg_blk == 0 ? 0 : seg_blk - 1; rem = nk2; }
-      } else {
-        if (seg_blk + 2 < nb) { op = 1; seg_blk += 2; rem = nk1; }
-        else { seg_blk += 1; rem = nk2; }
-      }
+      w.next();
+      int k;
+      int64_t blk;
+      if (w.b <= nb) w.cur(op, blk, k);
     };
     if (g == 1) step();
     int sl = g, ts = g;                            // ring slot / TMEM stage of this group's stage
@@ -648,8 +676,10 @@ static PFN_encode2_t pair_encode_fn() {
 }
 
 bool pair_supported(const View& v, int l) {
+  // opt-in (RTK_PAIR=1): measured slower than the one-CTA engine on C5 (1 MB pair-blocks double the
+  // L2 reuse footprint and op2's re-reads then miss to HBM: 8.2 GB per step instead of 4.4 GB)
   const char* e = getenv("RTK_PAIR");
-  if (e && e[0] == '0') return false;
+  if (!(e && e[0] == '1')) return false;
   const int N = tc_npad(l);
   if (!N) return false;
   if (!(v.P == 1 && v.si == 1 && v.ss >= v.n && v.ss % 4 == 0 && ((uintptr_t)v.base % 16) == 0)) return false;
@@ -700,6 +730,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   PairArgs a;
   a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + kPKS - 1) / kPKS; a.nblk = nblk;
   a.Ypart = Ypart; a.stop = stop;
+  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : 12;
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
   CUtensorMap tq, ta, ta2;
   memset(&tq, 0, sizeof(tq));
@@ -752,7 +783,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   }
 #endif
   const char* se = getenv("RTK_PAIR_SA");
-  const bool sa3 = !(se && se[0] == '2');
+  const bool sa3 = se && se[0] == '3';   // SA = 3 needs op1(b) to start after W(b-1) was drained
   switch (N) {
     case 16: return sa3 ? pair_launch<16, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<16, 2>(tq, ta, ta2, a, 2 * pairs, st);
     case 32: return sa3 ? pair_launch<32, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<32, 2>(tq, ta, ta2, a, 2 * pairs, st);

@@ -1,4 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "fused" 2>&1 | tail -2
-for i in 1 2; do timeout 60 python scripts/one_power_step.py 1000 1000000 60 20; done
-RTK_PAIR=0 timeout 60 python scripts/one_power_step.py 1000 1000000 60 20
-timeout 120 python scripts/prof_solve.py c5 3
+export RTUCKER_LIB=$PWD/paper_2506_04840_b200/librtucker_prof.so
+RTK_FUSED_DBG=4 timeout 60 python scripts/one_power_step.py 1000 1000000 60 2 2>&1 | tail -3
+RTK_FUSED_DBG=6 timeout 60 python scripts/one_power_step.py 1000 1000000 60 2 2>&1 | tail -3
+RTK_FUSED_DBG=68 timeout 60 python scripts/one_power_step.py 1000 1000000 60 2 2>&1 | tail -3
