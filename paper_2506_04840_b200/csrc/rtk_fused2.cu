@@ -78,43 +78,39 @@ struct PairArgs {
   int64_t nblk;    // pair-blocks: ceil(m / 256)
   float* Ypart;    // [P][N][nt * 256]
   const int* stop; // Alg. B.1 stop flag (nullptr: none)
-  int lag;         // op1-only stages at the start of each step (PWalk::L)
+  int lag;         // op1(b+1) stages issued before op2(b) (the lagged order, PSeg)
   int dbg;         // ablations (RTK_PAIR_DBG, timing only, results wrong): 1 no MMAs, 2 no A loads,
                    // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads
 };
 
-// Stage order shared by the TMA, MMA and producer warps.  Step 0 = op1(0); step b (1 <= b < nb)
-// = the first L stages of op1(b), then op2(b-1) and the rest of op1(b) alternating stage by stage,
-// then whichever is left; step nb = op2(nb-1).  op2(b) thus re-reads block b about one step after
-// op1(b) read it (the pair-blocks in flight, 74 x 1 MB per step, stay inside the 126 MB L2; with
-// op1(b+1) and op2(b) back to back the reuse distance was 1.5 steps and every op2 tile missed),
-// and the L op1-only stages cover the W exchange / op2-plane latency before op2(b-1) needs them.
-struct PWalk {
+// Stage order shared by the TMA, MMA and producer warps ("lagged" order):
+//   op1(0)[0:L], then for each block b:  op1(b)[L:nk1], op1(b+1)[0:L], op2(b)
+// op2(b) re-reads block b right after op1(b) finished it -- only op1(b+1)'s first L stages (which
+// cover the W(b) exchange / op2-plane latency) sit in between -- so most of a 1 MB pair-block is
+// re-read within ~L stages and the pair-blocks in flight stay far below the L2 size.  With the
+// order op1(b+1), op2(b) the reuse distance was 1.5 blocks (74 pairs x 1.5 MB > the usable L2)
+// and op2's re-reads missed to HBM: 8.2 GB per C5 step instead of 4.4 GB.
+// Segment walker for the warps that only need the op of each stage (the producers):
+struct PSeg {
   int nk1, nk2, L;
-  int64_t nb;
-  int64_t b = 0;
-  int pos = 0, len = 0;
+  int64_t nb, b;
+  int sub;          // 0: op1(0)[0:L]; then per block 1: op1(b)[L:], 2: op1(b+1)[0:L], 3: op2(b)
+  int op, rem;
   __device__ void init(int nk1_, int nk2_, int L_, int64_t nb_) {
-    nk1 = nk1_; nk2 = nk2_; L = L_ < nk1_ ? L_ : nk1_; nb = nb_;
-    b = 0; pos = 0; len = nk1;
+    nk1 = nk1_; nk2 = nk2_; L = L_ < 0 ? 0 : (L_ > nk1_ ? nk1_ : L_); nb = nb_;
+    b = 0; sub = 0; op = 1; rem = L;
+    if (rem == 0) advance();
   }
-  __device__ void cur(int& op, int64_t& blk, int& k) const {
-    if (b == 0) { op = 1; blk = 0; k = pos; return; }
-    if (b == nb) { op = 2; blk = nb - 1; k = pos; return; }
-    if (pos < L) { op = 1; blk = b; k = pos; return; }
-    const int r = pos - L, mi = (nk1 - L) < nk2 ? (nk1 - L) : nk2;
-    if (r < 2 * mi) {
-      if (r & 1) { op = 1; blk = b; k = L + (r >> 1); }
-      else { op = 2; blk = b - 1; k = r >> 1; }
-    } else if (nk1 - L > nk2) { op = 1; blk = b; k = L + mi + (r - 2 * mi); }
-    else { op = 2; blk = b - 1; k = mi + (r - 2 * mi); }
+  __device__ void advance() {   // to the next non-empty segment
+    while (true) {
+      if (sub == 0) { sub = 1; op = 1; rem = nk1 - L; }
+      else if (sub == 1) { sub = 2; op = 1; rem = (b + 1 < nb) ? L : 0; }
+      else if (sub == 2) { sub = 3; op = 2; rem = nk2; }
+      else { ++b; sub = 1; op = 1; rem = (b < nb) ? nk1 - L : 0; if (b >= nb) return; }
+      if (rem > 0) return;
+    }
   }
-  __device__ void next() {
-    if (++pos < len) return;
-    ++b;
-    pos = 0;
-    len = (b == nb) ? nk2 : nk1 + nk2;
-  }
+  __device__ void step() { if (--rem <= 0) advance(); }
 };
 
 __device__ __forceinline__ uint32_t p_cluster_rank() {
@@ -325,6 +321,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   const int64_t pid = blockIdx.x >> 1, P = gridDim.x >> 1;
   const int64_t nb = (a.nblk > pid) ? (a.nblk - pid + P - 1) / P : 0;   // pair-blocks of this pair
   const int nk1 = a.nk1, nk2 = a.nt * kPK2;
+  const int lagL = a.lag < 0 ? 0 : (a.lag > nk1 ? nk1 : a.lag);   // op1(b+1) stages ahead of op2(b)
   const int64_t total = nb * (nk1 + nk2);
 
   // stage order (TMA, MMA and producer warps alike): op1(0), [op1(1)], op2(0), op1(2), op2(1), ..., op2(nb-1)
@@ -374,14 +371,21 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         }
         if (++sl == kPRA) { sl = 0; ph ^= 1; }
       };
-      PWalk w;
-      w.init(nk1, nk2, a.lag, nb);
-      for (int64_t st = 0; st < total; ++st, w.next()) {
-        int op, k;
-        int64_t blk;
-        w.cur(op, blk, k);
-        if (op == 1) load(1, kPKS * k, colbase(blk) + 128 * rank);   // all rows of this CTA's 128 columns
-        else load(2, 256 * (k / kPK2) + 128 * (int)rank, colbase(blk) + kPKS * (k % kPK2));
+      const int L = lagL;
+      auto seg1 = [&](int64_t blk, int k0, int k1) {   // all rows of this CTA's 128 columns
+        const int64_t y = colbase(blk) + 128 * rank;
+        for (int k = k0; k < k1; ++k) load(1, kPKS * k, y);
+      };
+      auto seg2 = [&](int64_t blk) {                    // this CTA's rows of each pair-tile x 256 columns
+        const int64_t c0 = colbase(blk);
+        for (int tt = 0; tt < a.nt; ++tt)
+          for (int kq = 0; kq < kPK2; ++kq) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+      };
+      if (nb > 0) seg1(0, 0, L);
+      for (int64_t b = 0; b < nb; ++b) {
+        seg1(b, L, nk1);
+        if (b + 1 < nb) seg1(b + 1, 0, L);
+        seg2(b);
       }
     }
   } else if (warp == 1) {
@@ -396,60 +400,67 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       uint32_t qph = 0;
       auto next_a = [&]() { if (++sa == SA) { sa = 0; aph ^= 1; } };
       const long long _tm0 = PCLK();
-      PWalk w;
-      w.init(nk1, nk2, a.lag, nb);
-      for (int64_t st = 0; st < total; ++st, w.next()) {
-        int op, k;
-        int64_t blk;
-        w.cur(op, blk, k);
-        if (op == 1) {   // op1(blk) stage k -> W buffer blk % NW
-          const int b = NW == 2 ? (int)(blk & 1) : 0;
-          if (k == 0) {
-            const int64_t wu = NW == 2 ? (blk >> 1) : blk;   // use count of buffer b
-            { const long long _t0 = PCLK(); p_wait_cluster(&w_empty[b], (uint32_t)((wu & 1) ^ 1)); PACC(5, _t0); }
-          }
-          { const long long _t0 = PCLK(); bar_wait2(&q_full[qsl], qph, &a_full[sa], aph); PACC(1, _t0); }
-          tc_fence_after();
-          if (p_elect_one()) {
-            const uint32_t d = 256u + (uint32_t)(b * N);
-            const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
-            const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
-            if (mma_on) {
-#pragma unroll
-              for (int k8 = 0; k8 < 4; ++k8)
-                p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
-                              qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (k | k8) != 0);
-            }
-            p_commit_one(&a_empty[sa]);
-            p_commit_one(&q_empty[qsl]);
-            if (k == nk1 - 1) p_commit_one(&w_full[b]);
-          }
-          __syncwarp();
-          if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
-        } else {         // op2(blk) stage k: pair-tile k / 8, K chunk k % 8
-          if (k == 0) {
-            { const long long _t0 = PCLK(); p_wait_cluster(&p_full, (uint32_t)(blk & 1)); PACC(4, _t0); }
-          }
-          { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
-          tc_fence_after();
-          if (p_elect_one()) {
-            const int t = k / kPK2, kq = k % kPK2;
-            const uint32_t d = (uint32_t)(t * N);
-            const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
-            if (mma_on) {
-#pragma unroll
-              for (int k8 = 0; k8 < 4; ++k8) {
-                const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
-                p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
-                              p0 + (uint64_t)((PL + boff) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
-              }
-            }
-            p_commit_one(&a_empty[sa]);
-            if (k == nk2 - 1) p_commit_one(&p_empty);
-          }
-          __syncwarp();
+      auto op1 = [&](int64_t blk, int k) {   // op1(blk) stage k -> W buffer blk % NW
+        const int b = NW == 2 ? (int)(blk & 1) : 0;
+        if (k == 0) {
+          const int64_t wu = NW == 2 ? (blk >> 1) : blk;   // use count of buffer b
+          { const long long _t0 = PCLK(); p_wait_cluster(&w_empty[b], (uint32_t)((wu & 1) ^ 1)); PACC(5, _t0); }
         }
+        { const long long _t0 = PCLK(); bar_wait2(&q_full[qsl], qph, &a_full[sa], aph); PACC(1, _t0); }
+        tc_fence_after();
+        if (p_elect_one()) {
+          const uint32_t d = 256u + (uint32_t)(b * N);
+          const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
+          const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+          if (mma_on) {
+#pragma unroll
+            for (int k8 = 0; k8 < 4; ++k8)
+              p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+                            qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (k | k8) != 0);
+          }
+          p_commit_one(&a_empty[sa]);
+          p_commit_one(&q_empty[qsl]);
+          if (k == nk1 - 1) p_commit_one(&w_full[b]);
+        }
+        __syncwarp();
+        if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
         next_a();
+      };
+      auto op2 = [&](int64_t blk) {           // op2(blk): pair-tile t, K chunk kq
+        { const long long _t0 = PCLK(); p_wait_cluster(&p_full, (uint32_t)(blk & 1)); PACC(4, _t0); }
+        for (int t = 0; t < a.nt; ++t) {
+          const uint32_t d = (uint32_t)(t * N);
+#pragma unroll 1
+          for (int kq = 0; kq < kPK2; ++kq) {
+            { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
+            tc_fence_after();
+            if (p_elect_one()) {
+              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+              if (mma_on) {
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8) {
+                  const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
+                  p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
+                                p0 + (uint64_t)((PL + boff) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
+                }
+              }
+              p_commit_one(&a_empty[sa]);
+            }
+            __syncwarp();
+            next_a();
+          }
+        }
+        if (p_elect_one()) p_commit_one(&p_empty);
+        __syncwarp();
+      };
+      const int L = lagL;
+      if (nb > 0)
+        for (int k = 0; k < L; ++k) op1(0, k);
+      for (int64_t b = 0; b < nb; ++b) {
+        for (int k = L; k < nk1; ++k) op1(b, k);
+        if (b + 1 < nb)
+          for (int k = 0; k < L; ++k) op1(b + 1, k);
+        op2(b);
       }
       if (p_elect_one()) p_commit_one(&y_full);
       __syncwarp();
@@ -468,16 +479,9 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const uint32_t tile1 = smem_addr(smR) + (uint32_t)lt * 128u;   // op1: row lt of the SW128 tile
     const uint32_t tile2 = smem_addr(smR) + (uint32_t)lt * 4u;     // op2: column lt of [32 c][128 i]
     const uint32_t sw = (uint32_t)(lt & 7);
-    PWalk w;
-    w.init(nk1, nk2, a.lag, nb);
-    int op = 1;
-    auto step = [&]() {
-      w.next();
-      int k;
-      int64_t blk;
-      if (w.b <= nb) w.cur(op, blk, k);
-    };
-    if (g == 1) step();
+    PSeg w;
+    w.init(nk1, nk2, lagL, nb);
+    if (g == 1) w.step();
     int sl = g, ts = g;                            // ring slot / TMEM stage of this group's stage
     uint32_t rph = 0, tph = 0;
     const long long _tp0 = PCLK();
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         for (int c = 0; c < kPKS; ++c) v[c] = (float)(c + lt);
       } else
 #endif
-      if (op == 1) {
+      if (w.op == 1) {
         const uint32_t base = tile1 + (uint32_t)sl * kPTile;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -528,8 +532,8 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       if (sl >= kPRA) { sl -= kPRA; rph ^= 1u; }
       ts += 2;
       if (ts >= SA) { ts -= SA; tph ^= 1u; }
-      step();
-      step();
+      w.step();
+      w.step();
     }
     PACC(8, _tp0);
   } else if (warp < 14) {
@@ -676,10 +680,12 @@ static PFN_encode2_t pair_encode_fn() {
 }
 
 bool pair_supported(const View& v, int l) {
-  // opt-in (RTK_PAIR=1): measured slower than the one-CTA engine on C5 (1 MB pair-blocks double the
-  // L2 reuse footprint and op2's re-reads then miss to HBM: 8.2 GB per step instead of 4.4 GB)
+  // default for n_k > 256 (C3 / C5 mode 1): each CTA streams all rows of its 128 columns, which halves
+  // the B-operand and Q traffic per SM; for n_k <= 256 the one-CTA engine's 128-row tiles waste less
+  // (a pair-tile is 256 rows).  RTK_PAIR=0 / 1 forces it off / on.
   const char* e = getenv("RTK_PAIR");
-  if (!(e && e[0] == '1')) return false;
+  if (e && e[0] == '0') return false;
+  if (!(e && e[0] == '1') && v.n <= 256) return false;
   const int N = tc_npad(l);
   if (!N) return false;
   if (!(v.P == 1 && v.si == 1 && v.ss >= v.n && v.ss % 4 == 0 && ((uintptr_t)v.base % 16) == 0)) return false;
@@ -730,7 +736,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   PairArgs a;
   a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + kPKS - 1) / kPKS; a.nblk = nblk;
   a.Ypart = Ypart; a.stop = stop;
-  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : 12;
+  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : 8;
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
   CUtensorMap tq, ta, ta2;
   memset(&tq, 0, sizeof(tq));
