@@ -55,6 +55,9 @@ constexpr int kPK2 = kPBJ / kPKS;   // op2 stages per pair-tile (8)
 #ifndef RTK_PAIR_PROF
 #define RTK_PAIR_PROF 0
 #endif
+#ifndef RTK_PAIR_ABL   // -DRTK_PAIR_ABL=1: RTK_PAIR_DBG ablations without the role timers
+#define RTK_PAIR_ABL 0
+#endif
 #if RTK_PAIR_PROF
 __device__ unsigned long long g_pair_prof[2][32];
 #define PCLK() clock64()
@@ -273,6 +276,22 @@ __device__ __forceinline__ float lds32(uint32_t addr) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
+// both planes of a stage (hi at columns +0..31, lo at +32..63) in one 32x32b.x64 store
+__device__ __forceinline__ void p_tmem_st64(uint32_t taddr, const float (&v)[32], const float (&w)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,"
+      "%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]),
+      "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]), "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "f"(w[8]), "f"(w[9]),
+      "f"(w[10]), "f"(w[11]), "f"(w[12]), "f"(w[13]), "f"(w[14]), "f"(w[15]), "f"(w[16]), "f"(w[17]), "f"(w[18]),
+      "f"(w[19]), "f"(w[20]), "f"(w[21]), "f"(w[22]), "f"(w[23]), "f"(w[24]), "f"(w[25]), "f"(w[26]), "f"(w[27]),
+      "f"(w[28]), "f"(w[29]), "f"(w[30]), "f"(w[31])
+      : "memory");
+}
 __device__ __forceinline__ void p_tmem_st32(uint32_t taddr, const float (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
 
   pdl_wait();
   if (a.stop && *(volatile const int*)a.stop) return;   // uniform over the grid: before any barrier
-  const int dbg = RTK_PAIR_PROF ? a.dbg : 0;          // ablations exist only in profiling builds
+  const int dbg = (RTK_PAIR_PROF || RTK_PAIR_ABL) ? a.dbg : 0;   // ablations only in diagnostic builds
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = p_cluster_rank(), peer = rank ^ 1u;
   const bool leader = rank == 0;
@@ -488,7 +507,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     for (int64_t s = g; s < total; s += 2) {
       { const long long _t0 = PCLK(); bar_wait_addr(rfull0 + 8u * (uint32_t)sl, rph); PACC(9, _t0); }
       float v[kPKS];
-#if RTK_PAIR_PROF
+#if RTK_PAIR_PROF || RTK_PAIR_ABL
       if (dbg & 4) {
 #pragma unroll
         for (int c = 0; c < kPKS; ++c) v[c] = (float)(c + lt);
@@ -517,12 +536,11 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       { const long long _t0 = PCLK(); bar_wait_addr(aempty0 + 8u * (uint32_t)ts, tph ^ 1u); PACC(10, _t0); }
       tc_fence_after();
       const uint32_t tq = tq0 + (uint32_t)(2 * kPKS * ts);
-#if RTK_PAIR_PROF
+#if RTK_PAIR_PROF || RTK_PAIR_ABL
       if (!(dbg & 8))
 #endif
       {
-        p_tmem_st32(tq, v);
-        p_tmem_st32(tq + kPKS, lo);
+        p_tmem_st64(tq, v, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
