@@ -197,7 +197,7 @@ struct Layout {
   std::vector<char> tc_range, tc_shrink;
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
-  size_t g2part = 0, gsum = 0, amax = 0;
+  size_t g2part = 0, gsum = 0, amax = 0, lamx = 0;
   size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
   size_t om = 0, omtab = 0;                                         // Appendix D sketches only
   size_t mode_size = 0;   // bytes of one mode's scratch region (T-HOSVD: one region per mode)
@@ -299,6 +299,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.g2part = take((size_t)16 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);   // <= 16 cluster CTAs
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.amax = take((size_t)16 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 16 CTAs
+  L.lamx = take((size_t)kSolveLMax * 8);            // eigenvalues shared across the step cluster
   if (P.omega) {
     size_t oms = 0, tabs = 0;
     for (int k = 0; k < P.d; ++k) {
@@ -417,6 +418,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   B.g2part = (double*)(mw + L.g2part);
   B.gsum = (double*)(mw + L.gsum);
   B.amax = (double*)(mw + L.amax);
+  B.lamx = (double*)(mw + L.lamx);
   const bool fast = l <= kSolveLMax;   // cluster small solver (rtk_solve.cu)
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
   const uint32_t mode1 = (uint32_t)(k + 1);

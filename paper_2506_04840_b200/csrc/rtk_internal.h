@@ -77,6 +77,7 @@ struct ModeBufs {
   double* g2part = nullptr; // [8][np] second-pass Gram partials
   double* gsum = nullptr;   // [np]
   double* amax = nullptr;   // [8][128] sign-pin argmax exchange
+  double* lamx = nullptr;   // [64] eigenvalues exchanged across the cluster (final / B.1 steps)
 };
 
 cudaError_t launch_reduce_gram(const ModeBufs& B, bool power, cudaStream_t st);

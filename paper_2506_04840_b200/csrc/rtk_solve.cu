@@ -166,7 +166,7 @@ __device__ __forceinline__ double rcp_fast(double x) {
 // (b) threads (K, J > K) form R_KJ = R_KK^{-T} A_KJ and publish row block K to R; (c) every
 // (I, J > K) applies A_IJ -= R_KI^T R_KJ.  Two barriers per 4 columns.  Returns false
 // (uniformly) on a pivot <= 1e-13 * max(diag) or a non-finite pivot.
-__device__ bool chol_upper(const double* A, double* R, double* flag, int l) {
+__device__ __noinline__ bool chol_upper(const double* A, double* R, double* flag, int l) {
   const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
   double a[4][4];
   double dmax = 0.0;
@@ -268,7 +268,7 @@ __device__ bool chol_upper(const double* A, double* R, double* flag, int l) {
 // substitution, T12 by the product, the lower-left block zeroed).  rinv: kSL doubles of scratch.
 // T has leading dimension kMLD.  (Measured in the step kernel: 28k cycles against 39k for a 4 x 4
 // block-diagonal sweep; a recursive 8 -> 64 block version was no faster there.)
-__device__ void tri_inv_upper(const double* R, double* T, int l, double* rinv) {
+__device__ __noinline__ void tri_inv_upper(const double* R, double* T, int l, double* rinv) {
   (void)l;   // R is the identity beyond l, so is T
   const int tid = threadIdx.x;
   constexpr int H = kSL / 2;
@@ -338,7 +338,7 @@ __device__ void tri_inv_upper(const double* R, double* T, int l, double* rinv) {
 // registers, the same layout as A) and write it to QH (ld kLD) at the end: the eigenvectors of A are
 // then QH Z for those Z of the tridiagonal, one dense product instead of l - 2 reflector sweeps.
 template <bool ACC>
-__device__ void tridiag_t(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
+__device__ __noinline__ void tridiag_t(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
                           double* pvbuf, double* scal, double* QH) {
   const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
   const unsigned qm = 0xFu << ((tid & 31) & ~3);
@@ -491,7 +491,7 @@ __device__ __forceinline__ void tridiag(const double* A, int l, double* Hv, doub
 
 // Out(i, c) = sum_j QH(i, j) Z(j, c), i, c < l (all ld kLD): thread (i, part) computes columns
 // part + 4cc of row i.
-__device__ void qh_times_z(const double* QH, const double* Z, int l, double* Out) {
+__device__ __noinline__ void qh_times_z(const double* QH, const double* Z, int l, double* Out) {
   const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
   if (i < l) {
     double acc[16];
@@ -535,7 +535,7 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 
 // lambda_min of the tridiagonal by 256-point multisection: one log-spaced round over
 // [hi 2^-64, hi] (hi = min d_i >= lambda_min), then linear rounds to 1e-14 relative.
-__device__ double lambda_min_ms(const double* d, const double* e2, int l, int* ibuf, double* dbuf) {
+__device__ __noinline__ double lambda_min_ms(const double* d, const double* e2, int l, int* ibuf, double* dbuf) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     double hi = d[0];
@@ -574,7 +574,7 @@ __device__ double lambda_min_ms(const double* d, const double* e2, int l, int* i
 
 // All l eigenvalues (ascending, lam[c] = c-th smallest) by Sturm bisection: one 256-point
 // log-spaced scan over the Gershgorin range, then 4 threads per eigenvalue, 5-section rounds.
-__device__ void all_eigs(const double* d, const double* e, const double* e2, int l, double* lam, double* blo,
+__device__ __noinline__ void all_eigs(const double* d, const double* e, const double* e2, int l, double* lam, double* blo,
                          double* bhi, int* cnt) {
   const int tid = threadIdx.x;
   __shared__ double s_gl, s_gu;
@@ -639,10 +639,74 @@ __device__ void all_eigs(const double* d, const double* e, const double* e2, int
   __syncthreads();
 }
 
+// All l eigenvalues of the tridiagonal, split over the C CTAs of the step cluster: CTA `rank` owns
+// eigenvalues c = rank, rank + C, ... (at most ceil(l / C)) and refines each with P = kST / owned
+// threads by P-point multisection (P + 1 sub-intervals per round, ~log2(P) bits instead of the 2.3
+// of the 4-thread 5-section in all_eigs), same convergence rule as all_eigs; each eigenvalue is
+// computed by exactly one CTA (deterministic) and published to lamx, then every CTA reads all l
+// after a cluster barrier.  lam[c] = c-th smallest.  cnt: kST ints, blo / bhi: kSL doubles.
+__device__ __noinline__ void all_eigs_cluster(const double* d, const double* e, const double* e2, int l, double* lam,
+                                 double* blo, double* bhi, int* cnt, double* lamx, int rank, int C,
+                                 cg::cluster_group& cluster) {
+  const int tid = threadIdx.x;
+  __shared__ double s_gl, s_gu;
+  if (tid == 0) {
+    double gl = DBL_MAX, gu = -DBL_MAX;
+    for (int k = 0; k < l; ++k) {
+      const double r = (k > 0 ? fabs(e[k - 1]) : 0.0) + (k + 1 < l ? fabs(e[k]) : 0.0);
+      gl = fmin(gl, d[k] - r);
+      gu = fmax(gu, d[k] + r);
+    }
+    const double nrm = fmax(fabs(gl), fabs(gu));
+    s_gl = gl - 1e-14 * nrm - 1e-300;
+    s_gu = gu + 1e-14 * nrm + 1e-300;
+  }
+  const int ne = (l > rank) ? (l - rank + C - 1) / C : 0;   // eigenvalues this CTA owns
+  const int P = ne > 0 ? kST / ne : kST;                     // threads per eigenvalue
+  const int u = tid / P, s = tid % P;                        // owned eigenvalue u, multisection point s
+  const int c = rank + C * u;                                // its index (ascending)
+  const bool act = u < ne && c < l;
+  if (act && s == 0) { blo[u] = 0.0; bhi[u] = 0.0; }
+  __syncthreads();
+  const double gl = s_gl, gu = s_gu;
+  const double floor_abs = 4.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu));
+  if (act && s == 0) { blo[u] = gl; bhi[u] = gu; }
+  __syncthreads();
+  for (int round = 0; round < 24; ++round) {
+    int k = l + 1;
+    double lo = 0.0, hi = 0.0;
+    if (act) {
+      lo = blo[u];
+      hi = bhi[u];
+      const double mu = lo + (hi - lo) * ((double)(s + 1) / (double)(P + 1));
+      k = sturm_count(d, e2, l, mu);
+    }
+    cnt[tid] = k;
+    __syncthreads();
+    int done = 1;
+    if (act && s == 0) {
+      // the first point whose count exceeds c bounds the eigenvalue from above
+      int j = 0;
+      while (j < P && cnt[u * P + j] <= c) ++j;
+      const double w = hi - lo;
+      const double nlo = (j == 0) ? lo : lo + w * ((double)j / (double)(P + 1));
+      const double nhi = (j == P) ? hi : lo + w * ((double)(j + 1) / (double)(P + 1));
+      blo[u] = fmax(lo, nlo);
+      bhi[u] = fmin(hi, nhi);
+      done = (bhi[u] - blo[u]) <= fmax(1e-15 * fmax(fabs(blo[u]), fabs(bhi[u])), floor_abs) + 1e-300;
+    }
+    if (__syncthreads_and(done)) break;
+  }
+  if (act && s == 0) lamx[c] = 0.5 * (blo[u] + bhi[u]);
+  cluster.sync();
+  for (int i = tid; i < l; i += kST) lam[i] = __ldcg(lamx + i);
+  __syncthreads();
+}
+
 // Eigenvectors of the tridiagonal by inverse iteration (thread c < l: eigenvalue lam[c]); two
 // solves of (T - lam I) x = b with LU without pivoting (tiny pivots replaced by eps ||T||), a
 // deterministic start vector, normalised.  Z(i, c) = x_i.  LU pivots kept in Lu(i, c).
-__device__ void tri_eigvecs(const double* d, const double* e, const double* lam, int l, double* Z, double* Lu) {
+__device__ __noinline__ void tri_eigvecs(const double* d, const double* e, const double* lam, int l, double* Z, double* Lu) {
   const int c = threadIdx.x;
   if (c < l) {
     double tn = 0.0;
@@ -697,7 +761,7 @@ __device__ void tri_eigvecs(const double* d, const double* e, const double* lam,
 }
 
 // Z <- H_0 H_1 ... H_{l-3} Z  (H_k = I - beta_k v_k v_k^T on rows k+1..l-1), column-private quads.
-__device__ void back_transform(const double* Hv, const double* hb, int l, double* Z) {
+__device__ __noinline__ void back_transform(const double* Hv, const double* hb, int l, double* Z) {
   const int tid = threadIdx.x, c = tid >> 2, part = tid & 3;
   if (c < kSL) {
     for (int k = l - 3; k >= 0; --k) {
@@ -743,6 +807,7 @@ struct StepArgs {
   double pve_tol;           // > 0: Alg. B.1 stopping rule on power steps
   double* sighat;           // [kSL] B.1 sigma-hat of the previous power step (zero at mode start)
   int pin_q;                // Alg. A.2: U = sign-pinned Q (all l columns) and Qd pinned in place
+  double* lamx;             // [kSL] eigenvalue exchange across the cluster (global scratch)
 };
 
 struct StepSmem {
@@ -896,7 +961,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     tridiag(S.G, l, S.H, S.hb, S.d, S.e, S.pbuf, S.xrow, S.scal);
     for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
     __syncthreads();
-    all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+    all_eigs_cluster(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt, a.lamx, rank, C, cluster);
     if (tid == 0) {
       double dmax = 0.0;
       for (int i = 0; i < a.r; ++i)
@@ -977,7 +1042,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       for (int k = tid; k + 1 < l; k += kST) S.e2[k] = S.e[k] * S.e[k];
       __syncthreads();
       tck[ntck++] = clock64();
-      all_eigs(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt);
+      all_eigs_cluster(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt, a.lamx, rank, C, cluster);
       tck[ntck++] = clock64();
       tri_eigvecs(S.d, S.e, S.lam, l, S.H, S.R);   // tridiagonal's eigenvectors (Householder rows done)
       tck[ntck++] = clock64();
@@ -1638,6 +1703,7 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   a.pve_tol = pve_tol;
   a.sighat = B.sighat;
   a.pin_q = pin_q ? 1 : 0;
+  a.lamx = B.lamx;
   const int C = solve_cluster_size(B.n);
   const size_t smem = sizeof(StepSmem);
   cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
