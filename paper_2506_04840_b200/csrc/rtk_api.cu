@@ -456,7 +456,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
                            pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st, nullptr, 1, 1,
                            1, sk ? nullptr : stop, om));
-        g_launches += sk ? 1 : 0;
+        g_launches += (sk && !fused_sketch_gen(om)) ? 1 : 0;   // omega_planes_kernel
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
       } else {

@@ -122,6 +122,7 @@ cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketc
 
 // ---- fused single-pass power step (rtk_fused.cu) -----------------------------------
 int fused_cluster(int n);
+bool fused_sketch_gen(const float* om);   // fused sketch generates Omega in-kernel (no planes kernel)
 bool fused_supported(const View& v, int l);
 size_t fused_ypart_floats(const View& v, int l, int grid);
 cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
