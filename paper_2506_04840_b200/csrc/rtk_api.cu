@@ -191,6 +191,15 @@ View shrink_view(const Problem& P, int k, const float* A, const float* buf) {
   return v;
 }
 
+// the fused single-pass engine applies (RTK_FUSED=0: off, measurement)
+bool fused_ok(const View& v, int l) {
+  const char* fz = getenv("RTK_FUSED");
+  if (fz && fz[0] == '0') return false;
+  const char* pe = getenv("RTK_PATH");
+  if (pe && std::string(pe) == "ffma") return false;
+  return fused_supported(v, l);
+}
+
 struct Layout {
   size_t planes = 0, wbuf = 0;
   int64_t ldw = 0;
@@ -225,7 +234,8 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
     View svp = shrink_view(P, k, nullptr, nullptr);
     svp.base = k == 0 ? A : (const float*)nullptr;
     if (path != 1) {
-      L.tc_range[k] = tc_supported(rvp, l) ? 1 : 0;
+      // contiguous views: tcgen05 (fused or two-kernel); Alg. 3's strided views: the fused engine only
+      L.tc_range[k] = (rvp.P > 1 ? (l <= kSolveLMax && fused_ok(rvp, l)) : tc_supported(rvp, l)) ? 1 : 0;
       L.tc_shrink[k] = tc_supported(svp, P.keep[k]) ? 1 : 0;
     }
     if (L.tc_range[k]) {
@@ -352,7 +362,8 @@ const Layout& plan_cached(const Problem& P, int nsm, const float* A, int path) {
   add(P.d); add(P.p); add(P.q); add(P.seq); add(P.a2); add(P.omega); add(nsm); add(path);
   add((long long)((uintptr_t)A % 16));
   for (int k = 0; k < P.d; ++k) { add(P.dims[k]); add(P.ranks[k]); add(P.keep[k]); }
-  for (const char* ev : {"RTK_PATH", "RTK_PLAN", "RTK_PLAN_SKETCH", "RTK_PLAN_POWER", "RTK_PLAN_SHRINK"}) {
+  for (const char* ev : {"RTK_PATH", "RTK_PLAN", "RTK_PLAN_SKETCH", "RTK_PLAN_POWER", "RTK_PLAN_SHRINK", "RTK_FUSED",
+                         "RTK_FUSED_STRIDED"}) {
     const char* v = getenv(ev);
     key += v ? v : "-";
     key += ';';
@@ -422,10 +433,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   const bool fast = l <= kSolveLMax;   // cluster small solver (rtk_solve.cu)
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
   const uint32_t mode1 = (uint32_t)(k + 1);
-  const bool tc = L.tc_range[k] && tc_supported(v, l);
+  const bool strided = v.P > 1;
+  const bool tc = L.tc_range[k] && (strided ? (fast && fused_ok(v, l)) : tc_supported(v, l));
   Side* side = nullptr;
-  const char* fz = getenv("RTK_FUSED");
-  const bool fused = tc && fast && !(fz && fz[0] == '0') && fused_supported(v, l);   // single-pass power step
+  const bool fused = tc && fast && fused_ok(v, l);   // single-pass power step (strided views: always)
   const bool pve = P.pve > 0.0;   // Alg. B.1: the step kernel decides the stop, alpha inline
   const int* stop = pve ? B.status + 3 : nullptr;
   if (pve) RTK_CK(cudaMemsetAsync(B.sighat, 0, (size_t)l * sizeof(double), st));   // sigmahat = 0
@@ -450,7 +461,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       const int G = pending ? num_sms() - 1 : num_sms();   // leave the alpha_kernel its SM
       // sketch on the fused engine only for long unfoldings (Omega-plane generation has a fixed
       // cost; tc_op2 generates Omega in shared memory and is faster for small m)
-      if (fused && (step > 0 || v.m() >= fused_sketch_min())) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
+      if (fused && (step > 0 || strided || v.m() >= fused_sketch_min())) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
         int Gf = 0, rows = 0;
         const bool sk = step == 0;
         RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
