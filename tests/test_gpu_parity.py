@@ -174,6 +174,24 @@ def test_random_shapes(seq, dims, ranks, p, q):
     check(a, ranks, p, q, 77, seq, alpha_rtol=5e-3)
 
 
+@pytest.mark.parametrize("dims,ranks,p,q", [
+    ((32, 40, 30), (5, 6, 5), 4, 2),          # mode 2: P = 32 (four s slices per 128-column block)
+    ((64, 20, 50, 3), (6, 5, 6, 1), 2, 2),    # P = 64, 1280, 64000 (d = 4)
+    ((132, 30, 20), (10, 6, 5), 6, 3),        # P = 132: partial p-blocks padded with zero columns
+])
+def test_strided_views_on_fused_engine(dims, ranks, p, q, monkeypatch):
+    """Alg. 3's strided mode-k unfoldings (column j = p + P s) on the tcgen05 fused engine through
+    3-D tensor maps, against the oracle; RTK_FUSED_STRIDED=0 (FFMA tiles) gives the same answer."""
+    rng = np.random.default_rng(sum(dims) + 11)
+    cr = tuple(min(n, r + 3) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    re_f, re_o = check(a, ranks, p, q, 13, False, alpha_rtol=5e-3, ew_cols=0)
+    monkeypatch.setenv("RTK_FUSED_STRIDED", "0")
+    re_t, _ = check(a, ranks, p, q, 13, False, alpha_rtol=5e-3)
+    assert abs(re_f - re_t) <= 1e-4 * re_o
+
+
 @pytest.mark.parametrize("seq", [False, True])
 def test_exact_recovery_gpu(seq):
     """Rank-(3,4,2) Tucker tensor, l > rank: RE at float32 rounding level, orthonormal U
