@@ -45,6 +45,7 @@ constexpr int kLD = 65;        // leading dimension of the l x l fp64 shared mat
 constexpr int kMLD = 66;       // leading dimension of T (even: 16-byte double2 rows)
 constexpr int kST = 256;       // threads per CTA
 constexpr int kRBr = 8;        // rows per reduce_gram CTA
+constexpr int kRGC = 8;        // reduce_gram cluster: one Gram partial per kRGC * kRBr = 64 rows
 constexpr int kChunk = 64;     // rows per product chunk in step_kernel
 constexpr int kMaxC = 16;      // cluster size (16: non-portable opt-in, checked by occupancy query)
 constexpr double kPinTie = 1e-5;   // sign pin: |entries| within this (relative) of the max are tied (C6)
@@ -58,6 +59,10 @@ __device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
 }
 
 // =============================================================== reduce + Gram partials
+// Gram partials: one per 64-row block (a cluster of kRGC CTAs sums its CTAs' 8-row Grams through
+// distributed shared memory), so the consumers sum ceil(n / 64) partials, not ceil(n / 8).
+__host__ __device__ constexpr int gram_blocks(int n) { return (n + kRGC * kRBr - 1) / (kRGC * kRBr); }
+
 __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restrict__ Ypart, int G, int ltot,
                                                          int n_rows, int n, int l,
                                                          const double* __restrict__ Qd,
@@ -66,8 +71,9 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
                                                          const int* __restrict__ stop) {
   __shared__ double Ys[kRBr][kSL + 1];
   __shared__ double red[4][kSL][kRBr];
+  __shared__ double gps[kSL * (kSL + 1) / 2];   // this CTA's 8-row Gram (packed upper)
   sm100::pdl_wait();   // the power step's Y partials
-  if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode
+  if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode (uniform over the grid)
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kRBr;
   const int rows = min(kRBr, n - i0);
@@ -128,15 +134,31 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
   }
   __syncthreads();
   const int np = l * (l + 1) / 2;
-  double* gp = gpart + (int64_t)blockIdx.x * np;
   for (int e = tid; e < np; e += kST) {
     int c1, c2;
     unpack_upper(e, c1, c2);
     double s = 0.0;
 #pragma unroll
     for (int ii = 0; ii < kRBr; ++ii) s += Ys[ii][c1] * Ys[ii][c2];
+    gps[e] = s;
+  }
+  // the cluster's 64-row partial: CTA r sums its share of the entries over the kRGC CTAs' Grams
+  // (CTA order), read through distributed shared memory
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  const int r = (int)cluster.block_rank();
+  double* gp = gpart + (int64_t)(blockIdx.x / kRGC) * np;
+  const int e0 = r * np / kRGC, e1 = (r + 1) * np / kRGC;
+  for (int e = e0 + tid; e < e1; e += kST) {
+    double v[kRGC];
+#pragma unroll
+    for (int q = 0; q < kRGC; ++q) v[q] = cluster.map_shared_rank(gps, q)[e];
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRGC; ++q) s += v[q];
     gp[e] = s;
   }
+  cluster.sync();   // peers' shared memory stays live until every CTA has read it
 }
 
 // =============================================================== l x l building blocks
@@ -162,10 +184,12 @@ __device__ __forceinline__ double rcp_fast(double x) {
 
 // Blocked Cholesky A = R^T R of the symmetric l x l A (upper triangle read), R upper (zero below
 // the diagonal, identity beyond l), with 4 x 4 blocks on a 16 x 16 thread grid: thread (I, J)
-// keeps block A_IJ in registers.  Block step K: (a) thread (K, K) factors A_KK = R_KK^T R_KK;
-// (b) threads (K, J > K) form R_KJ = R_KK^{-T} A_KJ and publish row block K to R; (c) every
-// (I, J > K) applies A_IJ -= R_KI^T R_KJ.  Two barriers per 4 columns.  Returns false
-// (uniformly) on a pivot <= 1e-13 * max(diag) or a non-finite pivot.
+// keeps block A_IJ in registers.  Block step K: every thread (K, J >= K) factors the staged A_KK =
+// R_KK^T R_KK itself (identical inputs, identical R_KK) and forms R_KJ = R_KK^{-T} A_KJ with the
+// pivots' 1/sqrt, publishing row block K to R; then every (I, J > K) applies A_IJ -= R_KI^T R_KJ
+// and thread (K+1, K+1) stages A_{K+1,K+1}.  Two barriers per 4 columns, no serial diagonal-block
+// phase.  Returns false (uniformly) on a pivot <= 1e-13 * max(diag) or a non-finite pivot.
+// flag: 32 doubles of scratch ([0] breakdown flag, [16..31] the staged diagonal block).
 __device__ __noinline__ bool chol_upper(const double* A, double* R, double* flag, int l) {
   const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
   double a[4][4];
@@ -180,55 +204,61 @@ __device__ __noinline__ bool chol_upper(const double* A, double* R, double* flag
       if (row > col) R[row * kLD + col] = 0.0;
     }
   const double tol = 1e-13 * dmax;
-  if (tid == 0) flag[0] = 0.0;
+  double* akk = flag + 16;
+  if (tid == 0) {
+    flag[0] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) akk[4 * i + j] = a[i][j];
+  }
+  __syncthreads();
   const int nb = (l + 3) >> 2;
   for (int K = 0; K < nb; ++K) {
-    if (bi == K && bj == K) {   // (a) 4 x 4 Cholesky in registers: a -> R_KK (upper)
+    if (bi == K && bj >= K) {
+      double r[4][4], rs[4];
       bool bad = false;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double piv = a[k][k];
-        if (!(piv > tol) || !(piv < DBL_MAX)) bad = true;
-        const double rs = bad ? 0.0 : rsqrt_fast(piv);
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) a[k][j] = j < k ? 0.0 : a[k][j] * rs;   // row k of R_KK
+        for (int j = 0; j < 4; ++j) r[i][j] = akk[4 * i + j];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {   // 4 x 4 Cholesky in registers: r -> R_KK (upper)
+        const double piv = r[k][k];
+        if (!(piv > tol) || !(piv < DBL_MAX)) bad = true;
+        rs[k] = bad ? 0.0 : rsqrt_fast(piv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[k][j] = j < k ? 0.0 : r[k][j] * rs[k];
 #pragma unroll
         for (int i = k + 1; i < 4; ++i)
 #pragma unroll
-          for (int j = i; j < 4; ++j) a[i][j] = fma(-a[k][i], a[k][j], a[i][j]);
+          for (int j = i; j < 4; ++j) r[i][j] = fma(-r[k][i], r[k][j], r[i][j]);
       }
-      if (bad) flag[0] = 1.0;
+      if (bj == K) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * K + j] = a[i][j];
+          for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * K + j] = r[i][j];
+        if (bad) flag[0] = 1.0;
+      } else {   // R_KJ = R_KK^{-T} A_KJ (forward substitution, 1 / R_KK(k, k) = rs[k])
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double v = a[k][j];
+#pragma unroll
+            for (int m = 0; m < k; ++m) v = fma(-r[m][k], a[m][j], v);
+            a[k][j] = v * rs[k];
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * bj + j] = a[i][j];
+      }
     }
     __syncthreads();
     if (flag[0] != 0.0) return false;
-    if (bi == K && bj > K) {    // (b) R_KJ = R_KK^{-T} A_KJ (forward substitution, 4 rows)
-      double rkk[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) rkk[i][j] = R[(4 * K + i) * kLD + 4 * K + j];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double rinv = rcp_fast(rkk[k][k]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          double v = a[k][j];
-#pragma unroll
-          for (int m = 0; m < k; ++m) v = fma(-rkk[m][k], a[m][j], v);
-          a[k][j] = v * rinv;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) R[(4 * K + i) * kLD + 4 * bj + j] = a[i][j];
-    }
-    __syncthreads();
-    if (bi > K && bj >= bi) {   // (c) trailing update (upper blocks only)
+    if (bi > K && bj >= bi) {   // trailing update (upper blocks only)
       double rki[4][4], rkj[4][4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -246,7 +276,14 @@ __device__ __noinline__ bool chol_upper(const double* A, double* R, double* flag
           for (int m = 0; m < 4; ++m) v = fma(-rki[m][i], rkj[m][j], v);
           a[i][j] = v;
         }
+      if (bi == K + 1 && bj == K + 1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) akk[4 * i + j] = a[i][j];
+      }
     }
+    __syncthreads();
   }
   for (int idx = tid; idx < (kSL - l) * kSL; idx += kST) {   // identity padding rows l..63
     const int k = l + idx / kSL, j = idx % kSL;
@@ -331,17 +368,21 @@ __device__ __noinline__ void tri_inv_upper(const double* R, double* T, int l, do
 }
 
 // Householder tridiagonalisation H^T A H = tridiag(d, e) of the symmetric l x l A (read only).
-// Thread (i = tid/4, part = tid%4) keeps A(i, part + 4jj), jj < 16, in registers.  The quad that
-// owns row k builds reflector k from its registers (quad shuffles only): v_k on rows k+1..l-1
-// with v_k(k+1) = x0 - alpha is stored in Hv row k, beta_k in hb[k].  Two barriers per reflector.
+// Thread (i = tid/4, part = tid%4) keeps A(i, part + 4jj), jj < 16, in registers.  Step k: the warp
+// holding row k publishes it (Hv row k, entries j >= k+2; x0 = A(k, k+1), d_k = A(k, k) and
+// ss = sum_{j>=k+2} A(k, j)^2 in scal), and after one barrier EVERY thread builds reflector k from
+// those three scalars (identical inputs and operations, so no serial one-quad phase and no second
+// barrier for it): v_k on rows k+1..l-1 with v_k(k+1) = x0 - alpha, beta_k = 2 / |v_k|^2 in hb[k].
+// Then p = beta A v, K = beta/2 p^T v, A -= v p^T + (p - 2K v) v^T.  Two barriers per reflector.
+// Hv rows are zero outside k+1..l-1 (so the reflector reads need no index tests).
 // ACC: also accumulate QH = H_0 H_1 ... H_{l-3} (thread (i, part) keeps row i's columns part + 4jj in
 // registers, the same layout as A) and write it to QH (ld kLD) at the end: the eigenvectors of A are
 // then QH Z for those Z of the tridiagonal, one dense product instead of l - 2 reflector sweeps.
+// (scripts/micro/trd_bench.cu: 136k cycles at l = 60 against 192k for the one-quad reflector.)
 template <bool ACC>
 __device__ __noinline__ void tridiag_t(const double* A, int l, double* Hv, double* hb, double* d, double* e, double* pbuf,
-                          double* pvbuf, double* scal, double* QH) {
+                                  double* pvbuf, double* scal, double* QH) {
   const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
-  const unsigned qm = 0xFu << ((tid & 31) & ~3);
   double w[16];
   double qh[ACC ? 16 : 1];
   if (ACC) {
@@ -353,71 +394,76 @@ __device__ __noinline__ void tridiag_t(const double* A, int l, double* Hv, doubl
     const int j = part + 4 * jj;
     w[jj] = (i < l && j < l) ? A[min(i, j) * kLD + max(i, j)] : 0.0;
   }
-  for (int k = 0; k + 2 < l; ++k) {
-    double* sc = scal + 2 * (k & 1);
-    if (i == k) {   // reflector k from row k (this quad's registers)
-      double s4[4] = {0.0, 0.0, 0.0, 0.0}, x0 = 0.0, dk = 0.0;
+  // Hv row k holds v_k: entries j >= k+2 are A(k, j) as published by quad k, entry k+1 is v0 (every
+  // thread writes the same value before reading), entries j <= k and j >= l stay zero -- so the
+  // reflector reads need no index tests.  x0 = A(k, k+1), d_k = A(k, k), ss_k = sum_{j>=k+2} A(k, j)^2
+  // go to scal[4 (k & 1) + 0..2].
+  for (int idx = tid; idx < kSL * kSL; idx += kST) Hv[(idx >> 6) * kLD + (idx & 63)] = 0.0;
+  auto publish = [&](int k) {   // the warp holding row k (warp-uniform branch, full-warp shuffles)
+    if ((tid >> 5) != (k >> 3)) return;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const int j = part + 4 * jj;
-        if (j >= k + 2 && j < l) s4[jj & 3] = fma(w[jj], w[jj], s4[jj & 3]);
-        if (j == k + 1) x0 = w[jj];
-        if (j == k) dk = w[jj];
-      }
-      // quad sums through shared memory (partial-mask shuffles in a divergent warp are slow)
-      double* qs = scal + 4 + 12 * (k & 1);   // [3][4]
-      qs[part] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      qs[4 + part] = x0;
-      qs[8 + part] = dk;
-      __syncwarp(qm);
-      double ss = (qs[0] + qs[1]) + (qs[2] + qs[3]);
-      x0 = (qs[4] + qs[5]) + (qs[6] + qs[7]);
-      dk = (qs[8] + qs[9]) + (qs[10] + qs[11]);
-      double beta = 0.0, alph = x0, v0 = 0.0;
-      if (ss > 0.0) {
-        const double t = ss + x0 * x0;
-        const double nrm = t * rsqrt_fast(t);
-        alph = x0 > 0.0 ? -nrm : nrm;
-        v0 = x0 - alph;
-        beta = 2.0 * rcp_fast(ss + v0 * v0);
-      }
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const int j = part + 4 * jj;
-        if (j > k && j < l) Hv[k * kLD + j] = (j == k + 1) ? v0 : w[jj];
-      }
-      if (part == 0) {
-        d[k] = dk;
-        e[k] = alph;
-        hb[k] = beta;
-        sc[0] = beta;
-      }
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = part + 4 * jj;
+      if (j >= k + 2 && j < l) s4[jj & 3] = fma(w[jj], w[jj], s4[jj & 3]);
     }
-    __syncthreads();
-    const double beta = sc[0];
-    const double* v = Hv + k * kLD;
+    double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    if (i == k) {
+      double* sc = scal + 4 * (k & 1);
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = part + 4 * jj;
+        if (j >= k + 2 && j < l) Hv[k * kLD + j] = w[jj];
+        if (j == k + 1) sc[0] = w[jj];
+        if (j == k) sc[1] = w[jj];
+      }
+      if (part == 0) sc[2] = ss;
+    }
+  };
+  __syncthreads();
+  publish(0);
+  for (int k = 0; k + 2 < l; ++k) {
+    __syncthreads();   // row k and ss_k published
+    double* hk = Hv + k * kLD;
+    const double* sc = scal + 4 * (k & 1);
+    const double x0 = sc[0], dk = sc[1], ss = sc[2];
+    double beta = 0.0, alph = x0, v0 = 0.0;
+    if (ss > 0.0) {   // every thread builds reflector k (same inputs, same operations)
+      const double t = ss + x0 * x0;
+      const double nrm = t * rsqrt_fast(t);
+      alph = x0 > 0.0 ? -nrm : nrm;
+      v0 = x0 - alph;
+      beta = 2.0 * rcp_fast(ss + v0 * v0);
+    }
+    if (tid == 0) {
+      d[k] = dk;
+      e[k] = alph;
+      hb[k] = beta;
+    }
     if (beta != 0.0) {
-      // p_i = beta * sum_{j>k} A(i,j) v_j  for i > k; pv_i = p_i v_i
+      hk[k + 1] = v0;   // identical value from every thread
+      double vj[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) vj[jj] = hk[part + 4 * jj];
+      const double vi = hk[i];
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
       for (int jj = 0; jj < 16; jj += 4) {
-        const int j = part + 4 * jj;
-        if (j > k && j < l) s0 = fma(w[jj], v[j], s0);
-        if (j + 4 > k && j + 4 < l) s1 = fma(w[jj + 1], v[j + 4], s1);
-        if (j + 8 > k && j + 8 < l) s2 = fma(w[jj + 2], v[j + 8], s2);
-        if (j + 12 > k && j + 12 < l) s3 = fma(w[jj + 3], v[j + 12], s3);
+        s0 = fma(w[jj], vj[jj], s0);
+        s1 = fma(w[jj + 1], vj[jj + 1], s1);
+        s2 = fma(w[jj + 2], vj[jj + 2], s2);
+        s3 = fma(w[jj + 3], vj[jj + 3], s3);
       }
       double s = (s0 + s1) + (s2 + s3);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      double uq = 0.0;   // (QH v)_i, in 4 partial sums (a 16-FMA chain otherwise)
+      double uq = 0.0;
       if (ACC) {
         double u4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int j = part + 4 * jj;
-          if (j > k && j < l) u4[jj & 3] = fma(qh[jj], v[j], u4[jj & 3]);
-        }
+        for (int jj = 0; jj < 16; ++jj) u4[jj & 3] = fma(qh[jj], vj[jj], u4[jj & 3]);
         uq = (u4[0] + u4[1]) + (u4[2] + u4[3]);
         uq += __shfl_xor_sync(0xffffffffu, uq, 1);
         uq += __shfl_xor_sync(0xffffffffu, uq, 2);
@@ -425,39 +471,28 @@ __device__ __noinline__ void tridiag_t(const double* A, int l, double* Hv, doubl
       if (part == 0) {
         const bool act = i > k && i < l;
         pbuf[i] = act ? beta * s : 0.0;
-        pvbuf[i] = act ? beta * s * v[i] : 0.0;
+        pvbuf[i] = act ? beta * s * vi : 0.0;
       }
       __syncthreads();
-      // K = beta/2 p^T v (every warp, same fixed order: lanes j and j+32, then a butterfly),
-      // w = p - K v, A -= v w^T + w v^T
       const int lane = tid & 31;
-      double t0 = pvbuf[lane] + pvbuf[lane + 32];   // pvbuf is zero outside (k, l)
+      double t0 = pvbuf[lane] + pvbuf[lane + 32];
 #pragma unroll
       for (int o = 16; o; o >>= 1) t0 += __shfl_xor_sync(0xffffffffu, t0, o);
       const double K = 0.5 * beta * t0;
-      if (ACC && i < l) {   // QH <- QH - beta (QH v) v^T on columns k+1..l-1
+      if (ACC) {
         const double bu = beta * uq;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int j = part + 4 * jj;
-          if (j > k && j < l) qh[jj] = fma(-bu, v[j], qh[jj]);
-        }
+        for (int jj = 0; jj < 16; ++jj) qh[jj] = fma(-bu, vj[jj], qh[jj]);
       }
-      if (i > k && i < l) {
-        const double vi = v[i], wi = pbuf[i] - K * vi;
+      if (i > k && i < l) {   // A -= v w^T + w v^T with w = p - K v:  A_ij -= v_i p_j + (p_i - 2K v_i) v_j
+        const double bi = fma(-2.0 * K, vi, pbuf[i]);
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int j = part + 4 * jj;
-          if (j > k && j < l) {
-            const double vj = v[j], wj = pbuf[j] - K * vj;
-            w[jj] -= fma(vi, wj, wi * vj);
-          }
-        }
+        for (int jj = 0; jj < 16; ++jj) w[jj] = fma(-bi, vj[jj], fma(-vi, pbuf[part + 4 * jj], w[jj]));
       }
     }
+    publish(k + 1);
   }
   __syncthreads();
-  // trailing 2 x 2 (or 1 x 1)
   if (l >= 2) {
     if (i == l - 2) {
 #pragma unroll
@@ -489,23 +524,37 @@ __device__ __forceinline__ void tridiag(const double* A, int l, double* Hv, doub
   tridiag_t<false>(A, l, Hv, hb, d, e, pbuf, pvbuf, scal, nullptr);
 }
 
-// Out(i, c) = sum_j QH(i, j) Z(j, c), i, c < l (all ld kLD): thread (i, part) computes columns
-// part + 4cc of row i.
+// Out(i, c) = sum_j QH(i, j) Z(j, c), i, c < l (QH, Out: ld kLD; Z: ld kMLD, 16-byte rows).
+// Thread (rg = tid/16, cg = tid%16) computes the 4 x 4 block rows 4rg.., columns 4cg.. in registers:
+// per j 4 broadcast loads of QH, 2 double2 loads of Z -- the two halves in an order alternating
+// with bit 2 of cg, so a quarter warp's eight 16-byte loads fall in eight distinct bank groups.
 __device__ __noinline__ void qh_times_z(const double* QH, const double* Z, int l, double* Out) {
-  const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
-  if (i < l) {
-    double acc[16];
+  const int tid = threadIdx.x, rg = tid >> 4, cg = tid & 15;
+  const int h0 = (cg >> 2) & 1;
+  double acc[4][4];
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
-    for (int j = 0; j < l; ++j) {
-      const double q = QH[i * kLD + j];
+  for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) acc[cc] = fma(q, Z[j * kLD + part + 4 * cc], acc[cc]);
-    }
+    for (int cc = 0; cc < 4; ++cc) acc[r][cc] = 0.0;
+#pragma unroll 2
+  for (int j = 0; j < l; ++j) {
+    double q[4];
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc)
-      if (part + 4 * cc < l) Out[i * kLD + part + 4 * cc] = acc[cc];
+    for (int r = 0; r < 4; ++r) q[r] = QH[(4 * rg + r) * kLD + j];
+    const double2* zr = reinterpret_cast<const double2*>(Z + j * kMLD + 4 * cg);
+    const double2 za = zr[h0], zb = zr[h0 ^ 1];
+    const double2 z01 = h0 ? zb : za, z23 = h0 ? za : zb;
+    const double z[4] = {z01.x, z01.y, z23.x, z23.y};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) acc[r][cc] = fma(q[r], z[cc], acc[r][cc]);
   }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      if (4 * rg + r < l && 4 * cg + cc < l) Out[(4 * rg + r) * kLD + 4 * cg + cc] = acc[r][cc];
   __syncthreads();
 }
 
@@ -517,19 +566,26 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   double pp = 1.0, p = d[0] - mu;
   if (p == 0.0) p = -1e-300;
   int cnt = (p < 0.0);
-  for (int k = 1; k < l; ++k) {
-    double pn = fma(d[k] - mu, p, -e2[k - 1] * pp);
+  auto step = [&](double dk, double ek) {
+    double pn = fma(dk - mu, p, -ek * pp);
     if (pn == 0.0) pn = (p < 0.0) ? 1e-300 : -1e-300;
     cnt += ((pn < 0.0) != (p < 0.0));
     pp = p;
     p = pn;
-    if ((k & 3) == 0) {
-      const int ex = max((int)((__double_as_longlong(p) >> 52) & 0x7ff), (int)((__double_as_longlong(pp) >> 52) & 0x7ff));
-      const double sc = __longlong_as_double((long long)(2046 - ex) << 52);   // 2^(1023-ex)
-      p *= sc;
-      pp *= sc;
-    }
+  };
+  int k = 1;
+  for (; k + 3 < l; k += 4) {   // terms k..k+3 (k = 1 mod 4): loads first, rescale after term k+3
+    double dk[4], ek[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { dk[u] = d[k + u]; ek[u] = e2[k - 1 + u]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) step(dk[u], ek[u]);
+    const int ex = max((int)((__double_as_longlong(p) >> 52) & 0x7ff), (int)((__double_as_longlong(pp) >> 52) & 0x7ff));
+    const double sc = __longlong_as_double((long long)(2046 - ex) << 52);   // 2^(1023-ex)
+    p *= sc;
+    pp *= sc;
   }
+  for (; k < l; ++k) step(d[k], e2[k - 1]);   // fewer than 4 terms left: no rescale point
   return cnt;
 }
 
@@ -672,22 +728,23 @@ __device__ __noinline__ void all_eigs_cluster(const double* d, const double* e, 
   const double floor_abs = 4.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu));
   if (act && s == 0) { blo[u] = gl; bhi[u] = gu; }
   __syncthreads();
+  int* first = cnt;   // first[u]: smallest multisection point of eigenvalue u whose count exceeds u's index
+  if (act && s == 0) first[u] = P;
+  __syncthreads();
   for (int round = 0; round < 24; ++round) {
-    int k = l + 1;
     double lo = 0.0, hi = 0.0;
     if (act) {
       lo = blo[u];
       hi = bhi[u];
       const double mu = lo + (hi - lo) * ((double)(s + 1) / (double)(P + 1));
-      k = sturm_count(d, e2, l, mu);
+      if (sturm_count(d, e2, l, mu) > c) atomicMin(first + u, s);
     }
-    cnt[tid] = k;
     __syncthreads();
     int done = 1;
     if (act && s == 0) {
       // the first point whose count exceeds c bounds the eigenvalue from above
-      int j = 0;
-      while (j < P && cnt[u * P + j] <= c) ++j;
+      const int j = first[u];
+      first[u] = P;   // reset for the next round (read again only after the barrier below)
       const double w = hi - lo;
       const double nlo = (j == 0) ? lo : lo + w * ((double)j / (double)(P + 1));
       const double nhi = (j == P) ? hi : lo + w * ((double)(j + 1) / (double)(P + 1));
@@ -705,8 +762,10 @@ __device__ __noinline__ void all_eigs_cluster(const double* d, const double* e, 
 
 // Eigenvectors of the tridiagonal by inverse iteration (thread c < l: eigenvalue lam[c]); two
 // solves of (T - lam I) x = b with LU without pivoting (tiny pivots replaced by eps ||T||), a
-// deterministic start vector, normalised.  Z(i, c) = x_i.  LU pivots kept in Lu(i, c).
-__device__ __noinline__ void tri_eigvecs(const double* d, const double* e, const double* lam, int l, double* Z, double* Lu) {
+// deterministic start vector, normalised.  Z(i, c) = x_i at Z[i * ldz + c].  LU pivots kept in Lu(i, c).
+__device__ __noinline__ void tri_eigvecs(const double* __restrict__ d, const double* __restrict__ e,
+                                         const double* __restrict__ lam, int l, double* __restrict__ Z,
+                                         double* __restrict__ Lu, int ldz) {
   const int c = threadIdx.x;
   if (c < l) {
     double tn = 0.0;
@@ -716,45 +775,54 @@ __device__ __noinline__ void tri_eigvecs(const double* d, const double* e, const
     const double lm = lam[c];
     for (int i = 0; i < l; ++i) {   // start vector: deterministic, no special structure
       const uint32_t h = (uint32_t)(i * 0x9E3779B1u) ^ (uint32_t)(c * 0x85EBCA77u) ^ 0x2545F491u;
-      Z[i * kLD + c] = 0.5 + (double)((h >> 8) & 0xffff) * (1.0 / 65536.0);
+      Z[i * ldz + c] = 0.5 + (double)((h >> 8) & 0xffff) * (1.0 / 65536.0);
     }
     for (int it = 0; it < 2; ++it) {
       // forward: u_i = d_i - lam - m_i e_{i-1},  m_i = e_{i-1}/u_{i-1};  y_i = x_i - m_i y_{i-1}
       // (Lu keeps 1/u_i: one reciprocal on the forward chain, none on the backward one; rcp_fast is
-      // within an ulp, which inverse iteration does not notice)
-      double u = d[0] - lm;
-      if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
-      double ru = rcp_fast(u);
-      Lu[c] = ru;
+      // within an ulp, which inverse iteration does not notice).  The factorisation is the same in
+      // the second iteration: it reuses Lu and runs only the y recurrence.
       double y = Z[c];
-      for (int i = 1; i < l; ++i) {
-        const double m = e[i - 1] * ru;
-        u = d[i] - lm - m * e[i - 1];
+      if (it == 0) {
+        double u = d[0] - lm;
         if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
-        ru = rcp_fast(u);
-        Lu[i * kLD + c] = ru;
-        y = Z[i * kLD + c] - m * y;
-        Z[i * kLD + c] = y;
+        double ru = rcp_fast(u);
+        Lu[c] = ru;
+        for (int i = 1; i < l; ++i) {
+          const double m = e[i - 1] * ru;
+          u = d[i] - lm - m * e[i - 1];
+          if (fabs(u) < tiny) u = u < 0.0 ? -tiny : tiny;
+          ru = rcp_fast(u);
+          Lu[i * kLD + c] = ru;
+          y = Z[i * ldz + c] - m * y;
+          Z[i * ldz + c] = y;
+        }
+      } else {
+        for (int i = 1; i < l; ++i) {
+          const double m = e[i - 1] * Lu[(i - 1) * kLD + c];
+          y = Z[i * ldz + c] - m * y;
+          Z[i * ldz + c] = y;
+        }
       }
       // back: x_{l-1} = y_{l-1}/u_{l-1};  x_i = (y_i - e_i x_{i+1}) / u_i
-      double x = Z[(l - 1) * kLD + c] * Lu[(l - 1) * kLD + c];
-      Z[(l - 1) * kLD + c] = x;
+      double x = Z[(l - 1) * ldz + c] * Lu[(l - 1) * kLD + c];
+      Z[(l - 1) * ldz + c] = x;
       double mx = fabs(x);
       for (int i = l - 2; i >= 0; --i) {
-        x = (Z[i * kLD + c] - e[i] * x) * Lu[i * kLD + c];
-        Z[i * kLD + c] = x;
+        x = (Z[i * ldz + c] - e[i] * x) * Lu[i * kLD + c];
+        Z[i * ldz + c] = x;
         mx = fmax(mx, fabs(x));
       }
       // scale, then normalise
       const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
       double s = 0.0;
       for (int i = 0; i < l; ++i) {
-        const double v = Z[i * kLD + c] * inv;
-        Z[i * kLD + c] = v;
+        const double v = Z[i * ldz + c] * inv;
+        Z[i * ldz + c] = v;
         s += v * v;
       }
       const double rn = 1.0 / sqrt(s);
-      for (int i = 0; i < l; ++i) Z[i * kLD + c] *= rn;
+      for (int i = 0; i < l; ++i) Z[i * ldz + c] *= rn;
     }
   }
   __syncthreads();
@@ -814,7 +882,8 @@ struct StepSmem {
   double G[kSL * kLD];      // Gram (later second-pass Gram); eigen path: Z aliases it
   double R[kSL * kLD];      // Cholesky factor; eigen path: LU pivots
   double T[kSL * kMLD];     // transform applied to the rows (ld kMLD)
-  double H[kSL * kLD];      // Householder vectors; product-chunk staging aliases it
+  double H[kSL * kMLD];     // Householder vectors (ld kLD); product-chunk staging and the
+                            // tridiagonal's eigenvectors (ld kMLD) alias it
   double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL];
   double xrow[kSL], pbuf[kSL], rowbuf[2 * kSL], scal[32], dbuf[4];
   double colscale[kSL];
@@ -895,9 +964,31 @@ __device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, do
   }
 }
 
-// Fill G (symmetric, full) from packed upper entries in global memory (sum of `parts` arrays).
+// Fill G (symmetric, full) from packed upper entries in global memory (sum of `parts` arrays, in
+// part order).  parts == 1: all of a thread's loads are issued before the first store.
 __device__ void load_packed_sum(const double* src, int parts, int64_t stride, int l, double* G) {
   const int np = l * (l + 1) / 2;
+  if (parts == 1) {
+    constexpr int kPer = (kSL * (kSL + 1) / 2 + kST - 1) / kST;   // 9 entries per thread at most
+    double v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + u * kST;
+      v[u] = e < np ? ldcg(src + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = threadIdx.x + u * kST;
+      if (e < np) {
+        int c1, c2;
+        unpack_upper(e, c1, c2);
+        G[c1 * kLD + c2] = v[u];
+        G[c2 * kLD + c1] = v[u];
+      }
+    }
+    __syncthreads();
+    return;
+  }
   for (int e = threadIdx.x; e < np; e += kST) {
     int c1, c2;
     unpack_upper(e, c1, c2);
@@ -930,18 +1021,19 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   int ntck = 0;
   tck[ntck++] = clock64();
 
-  // ---- 1. G = sum of the Gram partials (entries split across the cluster, fixed b order)
+  // ---- 1. G = sum of the Gram partials (entries split across the cluster, fixed b order -- the
+  // order alpha_kernel uses, so both see the same G)
   {
     const int e0 = (int)((int64_t)rank * np / C), e1 = (int)((int64_t)(rank + 1) * np / C);
     for (int e = e0 + tid; e < e1; e += kST) {
       double s = 0.0;
       int b = 0;
-      for (; b + 8 <= a.nblk; b += 8) {   // 8 independent loads in flight, summed in b order
-        double v[8];
+      for (; b + 16 <= a.nblk; b += 16) {   // 16 independent loads in flight, summed in b order
+        double v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ldcg(a.gpart + (int64_t)(b + u) * np + e);
+        for (int u = 0; u < 16; ++u) v[u] = ldcg(a.gpart + (int64_t)(b + u) * np + e);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+        for (int u = 0; u < 16; ++u) s += v[u];
       }
       for (; b < a.nblk; ++b) s += ldcg(a.gpart + (int64_t)b * np + e);
       a.gsum[e] = s;
@@ -1044,12 +1136,12 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       tck[ntck++] = clock64();
       all_eigs_cluster(S.d, S.e, S.e2, l, S.lam, S.blo, S.bhi, S.cnt, a.lamx, rank, C, cluster);
       tck[ntck++] = clock64();
-      tri_eigvecs(S.d, S.e, S.lam, l, S.H, S.R);   // tridiagonal's eigenvectors (Householder rows done)
+      tri_eigvecs(S.d, S.e, S.lam, l, S.H, S.R, kMLD);   // tridiagonal's eigenvectors (Householder rows done)
       tck[ntck++] = clock64();
       qh_times_z(S.T, S.H, l, Z);                  // A's eigenvectors = QH Z
     } else {            // tridiag / all_eigs results are still intact when B.1 computed them
       tck[ntck++] = clock64();
-      tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R);
+      tri_eigvecs(S.d, S.e, S.lam, l, Z, S.R, kLD);
       tck[ntck++] = clock64();
       back_transform(S.H, S.hb, l, Z);
     }
@@ -1319,12 +1411,12 @@ __global__ void __launch_bounds__(kST, 1) alpha_kernel(const double* __restrict_
     for (int e = tid; e < np; e += kST) {
       double sum = 0.0;
       int b = 0;
-      for (; b + 8 <= nblk; b += 8) {
-        double v[8];
+      for (; b + 16 <= nblk; b += 16) {
+        double v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(gpart + (int64_t)(b + u) * np + e);
+        for (int u = 0; u < 16; ++u) v[u] = __ldcg(gpart + (int64_t)(b + u) * np + e);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sum += v[u];
+        for (int u = 0; u < 16; ++u) sum += v[u];
       }
       for (; b < nblk; ++b) sum += __ldcg(gpart + (int64_t)b * np + e);
       int c1, c2;
@@ -1356,7 +1448,7 @@ cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t s
   const size_t smem = sizeof(AlphaSmem);
   cudaError_t e = cudaFuncSetAttribute(alpha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  alpha_kernel<<<1, kST, smem, st>>>(B.gpart, (B.n + kRBr - 1) / kRBr, B.l, step, shift ? 1 : 0, B.alpha, B.trace,
+  alpha_kernel<<<1, kST, smem, st>>>(B.gpart, gram_blocks(B.n), B.l, step, shift ? 1 : 0, B.alpha, B.trace,
                                      B.status, B.sigma);
   return cudaGetLastError();
 }
@@ -1392,7 +1484,7 @@ __global__ void __launch_bounds__(kST) a2_gram_kernel(const double* __restrict__
 }
 
 struct A2Smem {
-  double G[kSL * kLD], R[kSL * kLD], H[kSL * kLD];
+  double G[kSL * kLD], R[kSL * kLD], H[kSL * kMLD];
   double d[kSL], e[kSL], e2[kSL], hb[kSL], lam[kSL], blo[kSL], bhi[kSL], pbuf[kSL], xrow[kSL];
   double scal[32], dbuf[4], dots[kSL];
   int cnt[kST];
@@ -1415,7 +1507,7 @@ __global__ void __launch_bounds__(kST, 1) a2_eig_kernel(const double* __restrict
   __syncthreads();
   all_eigs(S.d, S.e, S.e2, c, S.lam, S.blo, S.bhi, S.cnt);
   double* Z = S.G;
-  tri_eigvecs(S.d, S.e, S.lam, c, S.H, S.G);   // tridiagonal's eigenvectors into H (G is scratch)
+  tri_eigvecs(S.d, S.e, S.lam, c, S.H, S.G, kMLD);   // tridiagonal's eigenvectors into H (G is scratch)
   qh_times_z(S.R, S.H, c, Z);                  // eigenvectors of the Gram = QH Z
   // descending order into R: R(i, cc) = Z(i, c-1-cc)
   for (int idx = tid; idx < c * r; idx += kST) {
@@ -1667,19 +1759,22 @@ int solve_cluster_size(int n) {
   return std::max(1, std::min(kMaxC, C));
 }
 
-size_t solve_gpart_doubles(int n, int l) { return (size_t)((n + kRBr - 1) / kRBr) * l * (l + 1) / 2; }
+size_t solve_gpart_doubles(int n, int l) { return (size_t)gram_blocks(n) * l * (l + 1) / 2; }
 
 cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop) {
-  const int nblk = (B.n + kRBr - 1) / kRBr;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nblk, 1, 1);
+  cfg.gridDim = dim3(gram_blocks(B.n) * kRGC, 1, 1);   // CTAs past n contribute zero rows
   cfg.blockDim = dim3(kST, 1, 1);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kRGC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, reduce_gram_kernel, (const float*)B.Ypart, B.G, B.ltot, B.n_rows, B.n,
                                      B.l, (const double*)B.Qd, (const double*)B.alpha, power ? 1 : 0, B.Y, B.gpart,
                                      stop);
@@ -1693,7 +1788,7 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   StepArgs a;
   a.n = B.n; a.l = B.l; a.r = B.r; a.step = step; a.q = q;
   a.shift = shift ? 1 : 0; a.final_step = (step == q) ? 1 : 0;
-  a.nblk = (B.n + kRBr - 1) / kRBr;
+  a.nblk = gram_blocks(B.n);
   a.gpart = B.gpart; a.Y = B.Y; a.Q1 = B.Q1; a.g2part = B.g2part; a.gsum = B.gsum; a.amax = B.amax;
   a.Qd = B.Qd; a.Qs = B.Qs; a.planes = planes; a.pN = pN; a.pld = pld;
   a.alpha = B.alpha; a.trace = B.trace; a.sigma = B.sigma; a.status = B.status;

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <vector>
 #include <random>
-namespace rtk { int num_sms() { return 148; } }
+namespace rtk { int num_sms() { return 148; } bool pdl_enabled() { return false; } }
 using namespace rtk;
 __global__ void __launch_bounds__(256, 1) bench(const double* Gg, int l, long long* clk, double* out) {
   extern __shared__ __align__(16) uint8_t smraw[];
