@@ -84,6 +84,11 @@ struct PairArgs {
   int lag;         // op1(b+1) stages issued before op2(b) (the lagged order, PSeg)
   int dbg;         // ablations (RTK_PAIR_DBG, timing only, results wrong): 1 no MMAs, 2 no A loads,
                    // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads
+  int shrink;      // 1: the mode-k shrink G x_k U_k^T -- op1 only (W = M_J^T U), each CTA writes its
+                   // 128 columns' W rows as the next unfolding (no exchange, no op2, no Y)
+  float* out;      // shrink output (column-major, leading dimension ldnext)
+  int64_t Rprev, nnext, ldnext;
+  int lk;          // shrink: output columns (r_k <= N)
 };
 
 // Stage order shared by the TMA, MMA and producer warps ("lagged" order):
@@ -334,6 +339,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   pdl_wait();
   if (a.stop && *(volatile const int*)a.stop) return;   // uniform over the grid: before any barrier
   const int dbg = (RTK_PAIR_PROF || RTK_PAIR_ABL) ? a.dbg : 0;   // ablations only in diagnostic builds
+  const bool SHR = a.shrink != 0;   // op1 only (a.nt == 0: no op2 stages, no Y)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = p_cluster_rank(), peer = rank ^ 1u;
   const bool leader = rank == 0;
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
           bar_arrive(&r_full[sl]);
         } else {
           bar_expect_tx(&r_full[sl], kPTile);
-          if (op == 1) p_tma_load(dst, &tmA, x, (int)y, &r_full[sl], pol_keep);   // [128 j][32 i], SW128
+          if (op == 1) p_tma_load(dst, &tmA, x, (int)y, &r_full[sl], SHR ? pol_drop : pol_keep);   // [128 j][32 i], SW128
           else p_tma_load(dst, &tmA2, x, (int)y, &r_full[sl], pol_drop);         // [32 c][128 i]
         }
         if (++sl == kPRA) { sl = 0; ph ^= 1; }
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         for (int k = L; k < nk1; ++k) op1(b, k);
         if (b + 1 < nb)
           for (int k = 0; k < L; ++k) op1(b + 1, k);
-        op2(b);
+        if (!SHR) op2(b);
       }
       if (p_elect_one()) p_commit_one(&y_full);
       __syncwarp();
@@ -579,6 +585,24 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       tc_fence_before();
       __syncwarp();
       if (lane == 0) p_arrive_cluster(wempty_c[b]);
+      if (SHR) {
+        // G x_k U_k^T: W(j, c) = sum_i M(i, j) U(i, c) is entry (c, j) of the shrunk unfolding; write
+        // it at its place in the (k+1)-unfolding (Rprev x nnext x rest), rows padded to ldnext
+        const int64_t col = colbase(jb) + 128 * (int64_t)rank + j;
+        if (col < a.m) {
+          const int64_t aa = col % a.Rprev, tmp = col / a.Rprev;
+          const int64_t bb = tmp % a.nnext, cc = tmp / a.nnext;
+          const int64_t cs = a.ldnext * a.Rprev;   // entry (c, col) at o[cs c]
+          float* o = a.out + bb + a.ldnext * (aa + a.Rprev * (int64_t)a.lk * cc);
+#pragma unroll
+          for (int c = 0; c < N; ++c)
+            if (c < a.lk) o[cs * c] = w[c];
+          if (bb == a.nnext - 1 && a.ldnext > a.nnext)   // zero the row padding of this column
+            for (int cr = 0; cr < a.lk; ++cr)
+              for (int64_t z = 1; z < a.ldnext - a.nnext + 1; ++z) o[cs * cr + z] = 0.f;
+        }
+        continue;
+      }
       // exchange: the peer's N-half of my column j goes to the peer's rbuf row j; I receive the
       // peer's column j, my N-half.  Row j's 16-B chunk c4 sits at (c4 + j) mod N2/4 so that the
       // reads below are bank-conflict-free.
@@ -631,7 +655,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     // ---- final: this CTA's Y rows (its half of every pair-tile) -> Ypart[pair][c][row]
     const int rows_tot = a.nt * 256;
     float* yp = a.Ypart + pid * (int64_t)N * rows_tot;
-    if (nb > 0) {
+    if (nb > 0 && !SHR) {
       p_wait_sleep(&y_full, 0);
       tc_fence_after();
     }
@@ -745,8 +769,9 @@ static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, con
 // One power step Y = M M^T Q on the pair engine from Q's hi/lo planes [2N][pld].
 // Ypart[grid/2][N][nt*256]; returns the partial count and row pitch.
 cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
-                       int* rows_out, cudaStream_t st, const int* stop) {
-  const int N = tc_npad(l), nt = (v.n + 255) / 256;
+                       int* rows_out, cudaStream_t st, const int* stop, float* shrink_out, int64_t Rprev,
+                       int64_t nnext, int64_t ldnext) {
+  const int N = tc_npad(l), nt = shrink_out ? 0 : (v.n + 255) / 256;
   const int64_t m = v.m();
   const int64_t nblk = (m + kPBJ - 1) / kPBJ;
   int pairs = std::max(1, grid / 2);
@@ -756,6 +781,10 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   a.Ypart = Ypart; a.stop = stop;
   a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : 8;
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
+  a.shrink = shrink_out ? 1 : 0;
+  a.out = shrink_out;
+  a.Rprev = Rprev; a.nnext = nnext; a.ldnext = ldnext;
+  a.lk = l;
   CUtensorMap tq, ta, ta2;
   memset(&tq, 0, sizeof(tq));
   memset(&ta, 0, sizeof(ta));

@@ -133,6 +133,30 @@ def test_fused_sketch_engine(seq, dims, ranks, p, q, monkeypatch):
     check(a, ranks, p, q, 77, seq, alpha_rtol=5e-3, ew_cols=0)
 
 
+@pytest.mark.parametrize("dims,ranks", [((600, 90, 81), (20, 10, 10)), ((1000, 130, 37), (50, 12, 8))])
+def test_pair_shrink_engine(dims, ranks, monkeypatch):
+    """The mode shrink G x_k U_k^T on the CTA-pair engine (n_k > 256: op1 only, each CTA writing its
+    128 columns' W rows into the next unfolding; ragged last pair-block, next unfolding's rows padded
+    n = 90 -> 92 / 130 -> 132): full oracle parity incl. core entries, and agreement with the one-CTA
+    engine's shrink (RTK_PAIR_SHRINK=0) to fp32 rounding."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import solve
+    rng = np.random.default_rng(sum(dims) + 7)
+    cr = tuple(min(n, r + 4) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) * np.exp(-0.25 * np.indices(cr).sum(axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    monkeypatch.setenv("RTK_PAIR_SHRINK", "1")
+    check(a, ranks, 6, 2, 31, True, ew_cols=0)
+    A = to_device_colmajor(a, torch)
+    core1, u1 = solve(A, ranks, 6, 2, 31, sequential=True)
+    monkeypatch.setenv("RTK_PAIR_SHRINK", "0")
+    core0, u0 = solve(A, ranks, 6, 2, 31, sequential=True)
+    c1, c0 = core1.double().cpu().numpy(), core0.double().cpu().numpy()
+    assert np.abs(c1 - c0).max() <= 2e-5 * np.abs(c0).max()
+    for a1, a0 in zip(u1, u0):
+        assert torch.allclose(a1, a0, atol=2e-5)
+
+
 def test_c5_launch_path_ci_size():
     """C5's recipe and parameters (r = 50, p = 10, q = 5) at 1000 x 400 x 300: mode 1 is n = 1000,
     l = 60, m = 1.2e5 >= 1e5, so the sketch takes the fused Omega-plane engine on the 2-CTA
