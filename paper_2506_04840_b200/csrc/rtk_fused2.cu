@@ -89,6 +89,8 @@ struct PairArgs {
   float* out;      // shrink output (column-major, leading dimension ldnext)
   int64_t Rprev, nnext, ldnext;
   int lk;          // shrink: output columns (r_k <= N)
+  int sketch;      // 1: the sketch Y = M Omega -- op2 only, B = the Omega planes streamed through the
+                   // Q ring one 32-column K chunk at a time (K chunk outer, pair-tile inner), no W
 };
 
 // Stage order shared by the TMA, MMA and producer warps ("lagged" order):
@@ -340,12 +342,13 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   if (a.stop && *(volatile const int*)a.stop) return;   // uniform over the grid: before any barrier
   const int dbg = (RTK_PAIR_PROF || RTK_PAIR_ABL) ? a.dbg : 0;   // ablations only in diagnostic builds
   const bool SHR = a.shrink != 0;   // op1 only (a.nt == 0: no op2 stages, no Y)
+  const bool SKT = a.sketch != 0;   // op2 only (no op1 stages, no W)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = p_cluster_rank(), peer = rank ^ 1u;
   const bool leader = rank == 0;
   const int64_t pid = blockIdx.x >> 1, P = gridDim.x >> 1;
   const int64_t nb = (a.nblk > pid) ? (a.nblk - pid + P - 1) / P : 0;   // pair-blocks of this pair
-  const int nk1 = a.nk1, nk2 = a.nt * kPK2;
+  const int nk1 = SKT ? 0 : a.nk1, nk2 = a.nt * kPK2;
   const int lagL = a.lag < 0 ? 0 : (a.lag > nk1 ? nk1 : a.lag);   // op1(b+1) stages ahead of op2(b)
   const int64_t total = nb * (nk1 + nk2);
 
@@ -403,8 +406,13 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       };
       auto seg2 = [&](int64_t blk) {                    // this CTA's rows of each pair-tile x 256 columns
         const int64_t c0 = colbase(blk);
-        for (int tt = 0; tt < a.nt; ++tt)
-          for (int kq = 0; kq < kPK2; ++kq) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+        if (SKT) {   // the MMA's sketch order: K chunk outer, pair-tile inner
+          for (int kq = 0; kq < kPK2; ++kq)
+            for (int tt = 0; tt < a.nt; ++tt) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+        } else {
+          for (int tt = 0; tt < a.nt; ++tt)
+            for (int kq = 0; kq < kPK2; ++kq) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+        }
       };
       if (nb > 0) seg1(0, 0, L);
       for (int64_t b = 0; b < nb; ++b) {
@@ -478,14 +486,45 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         if (p_elect_one()) p_commit_one(&p_empty);
         __syncwarp();
       };
+      auto op2s = [&](int64_t blk) {          // sketch op2(blk): K chunk kq (Omega, Q ring) x pair-tile t
+#pragma unroll 1
+        for (int kq = 0; kq < kPK2; ++kq) {
+          { const long long _t0 = PCLK(); bar_wait(&q_full[qsl], qph); PACC(2, _t0); }
+          const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
+#pragma unroll 1
+          for (int t = 0; t < a.nt; ++t) {
+            { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
+            tc_fence_after();
+            if (p_elect_one()) {
+              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+              if (mma_on) {
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8)
+                  p_mma3<IDESC>((uint32_t)(t * N), ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+                                qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
+              }
+              p_commit_one(&a_empty[sa]);
+            }
+            __syncwarp();
+            next_a();
+          }
+          if (p_elect_one()) p_commit_one(&q_empty[qsl]);
+          __syncwarp();
+          if (++qsl == kPRQ) { qsl = 0; qph ^= 1; }
+        }
+      };
       const int L = lagL;
-      if (nb > 0)
-        for (int k = 0; k < L; ++k) op1(0, k);
-      for (int64_t b = 0; b < nb; ++b) {
-        for (int k = L; k < nk1; ++k) op1(b, k);
-        if (b + 1 < nb)
-          for (int k = 0; k < L; ++k) op1(b + 1, k);
-        if (!SHR) op2(b);
+      if (SKT) {
+        for (int64_t b = 0; b < nb; ++b) op2s(b);
+      } else {
+        if (nb > 0)
+          for (int k = 0; k < L; ++k) op1(0, k);
+        for (int64_t b = 0; b < nb; ++b) {
+          for (int k = L; k < nk1; ++k) op1(b, k);
+          if (b + 1 < nb)
+            for (int k = 0; k < L; ++k) op1(b + 1, k);
+          if (!SHR) op2(b);
+        }
       }
       if (p_elect_one()) p_commit_one(&y_full);
       __syncwarp();
@@ -570,7 +609,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const uint32_t rbar = p_mapa(smem_addr(&x_full), peer);
     const uint32_t rcredit = p_mapa(smem_addr(&credit), peer);
     const long long _te0 = PCLK();
-    for (int64_t jb = 0; jb < nb; ++jb) {
+    for (int64_t jb = 0; jb < (SKT ? 0 : nb); ++jb) {
       const int b = NW == 2 ? (int)(jb & 1) : 0;
       { const long long _t0 = PCLK(); p_wait_sleep(&w_full[b], (uint32_t)((NW == 2 ? (jb >> 1) : jb) & 1)); PACC(21, _t0); }
       tc_fence_after();
@@ -682,17 +721,21 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const uint32_t qfull0 = p_mapa(smem_addr(&q_full[0]), 0);
     int sl = 0;
     uint32_t ph = 0;
+    // sketch: the K chunks of the Omega planes (columns colbase + 32 kq of the pair-block), read once
+    const uint64_t pol_q = SKT ? p_policy_first() : pol_keep;
+    const int nq = SKT ? kPK2 : nk1;
     for (int64_t jb = 0; jb < nb; ++jb)
-      for (int k = 0; k < nk1; ++k) {
+      for (int k = 0; k < nq; ++k) {
         { const long long _t0 = PCLK(); bar_wait(&q_empty[sl], ph ^ 1); PACC(24, _t0); }
         uint8_t* sq = smQ + sl * QS;
         const uint32_t cb = qfull0 + 8u * (uint32_t)sl;
+        const int x = SKT ? (int)(colbase(jb) + kPKS * k) : kPKS * k;
         if (dbg & 16) {
           if (leader) bar_arrive(&q_full[sl]);
         } else {
           if (leader) bar_expect_tx(&q_full[sl], 2 * QS);   // both CTAs' halves
-          p_tma_load_pair(sq, &tmQ, kPKS * k, (int)rank * N2, cb, pol_keep);
-          p_tma_load_pair(sq + N2 * 128, &tmQ, kPKS * k, N + (int)rank * N2, cb, pol_keep);
+          p_tma_load_pair(sq, &tmQ, x, (int)rank * N2, cb, pol_q);
+          p_tma_load_pair(sq + N2 * 128, &tmQ, x, N + (int)rank * N2, cb, pol_q);
         }
         if (++sl == kPRQ) { sl = 0; ph ^= 1; }
       }
@@ -770,7 +813,7 @@ static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, con
 // Ypart[grid/2][N][nt*256]; returns the partial count and row pitch.
 cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
                        int* rows_out, cudaStream_t st, const int* stop, float* shrink_out, int64_t Rprev,
-                       int64_t nnext, int64_t ldnext) {
+                       int64_t nnext, int64_t ldnext, bool sketch) {
   const int N = tc_npad(l), nt = shrink_out ? 0 : (v.n + 255) / 256;
   const int64_t m = v.m();
   const int64_t nblk = (m + kPBJ - 1) / kPBJ;
@@ -785,6 +828,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   a.out = shrink_out;
   a.Rprev = Rprev; a.nnext = nnext; a.ldnext = ldnext;
   a.lk = l;
+  a.sketch = sketch ? 1 : 0;
   CUtensorMap tq, ta, ta2;
   memset(&tq, 0, sizeof(tq));
   memset(&ta, 0, sizeof(ta));
@@ -808,8 +852,9 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  {   // Q planes [2N][pld]: box {32 rows i, N/2 columns c}, SWIZZLE_128B ([N/2 c][32 i])
-    cuuint64_t dims[2] = {(cuuint64_t)v.n, (cuuint64_t)(2 * N)};
+  {   // Q planes [2N][pld]: box {32 rows i, N/2 columns c}, SWIZZLE_128B ([N/2 c][32 i]); the sketch's
+      // Omega planes [2N][pld >= m] the same way with the unfolding's columns j in place of i
+    cuuint64_t dims[2] = {(cuuint64_t)(sketch ? m : v.n), (cuuint64_t)(2 * N)};
     cuuint64_t strides[1] = {(cuuint64_t)pld * 4};
     cuuint32_t box[2] = {32, (cuuint32_t)(N / 2)};
     if (pair_encode_fn()(&tq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(planes), dims, strides, box, es,

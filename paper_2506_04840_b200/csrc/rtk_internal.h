@@ -134,10 +134,11 @@ cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool
 bool pair_supported(const View& v, int l);
 size_t pair_ypart_floats(const View& v, int l, int grid);
 // shrink_out != nullptr: the mode shrink G x_k U_k^T instead (op1 only, planes = U's, l = r_k),
-// written as the next unfolding (Rprev, nnext, ldnext as in TileLaunch)
+// written as the next unfolding (Rprev, nnext, ldnext as in TileLaunch).  sketch: Y = M Omega_k
+// (op2 only) with planes = the Omega planes [2N][pld >= m] of omega_planes_kernel.
 cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
                        int* rows_out, cudaStream_t st, const int* stop, float* shrink_out = nullptr,
-                       int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1);
+                       int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1, bool sketch = false);
 
 // ---- Appendix D sketch types (rtk_omega.cu) ------------------------------------------
 // Materialise Omega_k rows [row0, row0 + rows) x l (row-major [j][l]) of the given type for the

@@ -115,16 +115,20 @@ def test_config_parity(cfg, path, monkeypatch):
     check(a, c["ranks"], c["p"], c["q"], c["omega_seed"], c["algo"] == "rsthosvd", ew_cols=EW_COLS[cfg])
 
 
+@pytest.mark.parametrize("engine", ["pair", "cta"])
 @pytest.mark.parametrize("seq", [False, True])
 @pytest.mark.parametrize("dims,ranks,p,q", [
     ((640, 40, 36), (20, 8, 6), 6, 3),        # n_1 > 512: 2-CTA cluster
     ((1000, 30, 20), (30, 6, 5), 10, 2),      # n_1 = 1000, l = 40
     ((1000, 64, 40), (50, 10, 8), 10, 3),     # n_1 = 1000, l = 60 (N = 64): C5's mode-1 kernel shape
 ])
-def test_fused_sketch_engine(seq, dims, ranks, p, q, monkeypatch):
+def test_fused_sketch_engine(seq, dims, ranks, p, q, engine, monkeypatch):
     """The fused Omega-plane sketch (the engine C5's mode 1 sketch runs on, normally only for
-    m >= 1e5) forced on at small m with RTK_FUSED_SKETCH_MIN=0: oracle parity incl. alpha traces."""
+    m >= 1e5) forced on at small m with RTK_FUSED_SKETCH_MIN=0, on the CTA-pair engine (op2 only,
+    Omega K chunks through the Q ring; n_1 > 256 here) and on the one-CTA engine
+    (RTK_PAIR_SKETCH=0): oracle parity incl. alpha traces."""
     monkeypatch.setenv("RTK_FUSED_SKETCH_MIN", "0")
+    monkeypatch.setenv("RTK_PAIR_SKETCH", "1" if engine == "pair" else "0")
     rng = np.random.default_rng(sum(dims) + 101)
     cr = tuple(min(n, r + 3) for n, r in zip(dims, ranks))
     core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
