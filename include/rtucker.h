@@ -152,6 +152,34 @@ RTK_API int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dim
 RTK_API size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks,
                            int32_t p, int32_t q);
 
+/* ---- Multi-GPU: Alg. 4 with A split along its LAST mode ----------------------
+ *
+ * In-place sum of `count` elements (dtype 0: float32, 1: float64) of the DEVICE buffer `buf` over
+ * all ranks of the caller's group, ordered on `stream` (the work enqueued before the call produces
+ * buf, the work enqueued after it reads the sum).  Every rank must obtain bit-identical sums (NCCL
+ * and gloo all-reduce do).  Returns 0 on success. */
+typedef int (*rtk_allreduce_fn)(void* buf, int64_t count, int32_t dtype, void* stream, void* ctx);
+
+/* Alg. 4 (R-ST-HOSVD, sequential = 1, shift as opt->shift, variant 0, no PVE) on one rank of a
+ * group that holds A split along mode d: A_slab is this rank's column-major slab, extents
+ * dims[0..d-2] x last_count, covering indices [last_begin, last_begin + last_count) of mode d
+ * (dims[d-1] = the FULL extent; slabs of all ranks tile it).  For every mode k < d the slab is a
+ * contiguous range of the unfolding's columns (i_d is the slowest column index), so the rank
+ * streams its own columns (sketch against rows [j0, j0 + m) of Omega_k of the full problem, power
+ * steps, shrink) and `allreduce` sums the n_k x l_k Y after every streaming pass (float64; `root`
+ * != 0 on exactly one rank, which applies -alpha Q once); the small solves then run redundantly and
+ * bit-identically everywhere.  Before mode d the rank's shrunk slab is placed at its rows of the
+ * mode-d unfolding and all-reduced (float32, zero elsewhere), and mode d plus the core run
+ * redundantly.  Outputs as rtk_solve, identical on every rank.  The tensor is split, not
+ * replicated: each GPU holds 1 / world of it.  l_k <= 64 for k < d (RTK_ERR_ARG otherwise);
+ * ws: rtk_workspace_bytes_shard; NULL ws allocates with cudaMallocAsync. */
+RTK_API int rtk_rsthosvd_shard(const rtk_options* opt, const float* A_slab, const int64_t* dims, int32_t d,
+                               int64_t last_begin, int64_t last_count, int32_t root, const int32_t* ranks,
+                               int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws,
+                               size_t ws_bytes, void* stream, rtk_allreduce_fn allreduce, void* ctx);
+RTK_API size_t rtk_workspace_bytes_shard(const rtk_options* opt, const int64_t* dims, int32_t d,
+                                         int64_t last_count, const int32_t* ranks, int32_t p, int32_t q);
+
 /* Workspace bytes for rtk_solve with these options (NULL -> ST-HOSVD defaults); 0 on error. */
 RTK_API size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32_t d,
                                       const int32_t* ranks, int32_t p, int32_t q);

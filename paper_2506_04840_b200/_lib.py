@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 ABI_FUNCTIONS = ["rtk_rthosvd", "rtk_rsthosvd", "rtk_solve", "rtk_workspace_bytes", "rtk_workspace_bytes_ex",
-                 "rtk_omega", "rtk_sketch",
+                 "rtk_omega", "rtk_sketch", "rtk_rsthosvd_shard", "rtk_workspace_bytes_shard",
                  "rtk_power_step", "rtk_profile_begin", "rtk_profile_end", "rtk_debug_step_clocks",
                  "rtk_last_error", "rtk_version"]
 
@@ -40,6 +40,11 @@ class _Options(ctypes.Structure):
     _fields_ = [("sequential", ctypes.c_int32), ("shift", ctypes.c_int32),
                 ("pve_tol", ctypes.c_double), ("path", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("omega", ctypes.c_int32)]
+
+
+# rtk_allreduce_fn: int (*)(void* buf, int64_t count, int32_t dtype, void* stream, void* ctx)
+_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                 ctypes.c_void_p)
 
 
 def lib_path() -> str:
@@ -76,6 +81,14 @@ def load_library():
     lib.rtk_sketch.argtypes = [ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32, i64p, ctypes.c_int32,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
     lib.rtk_sketch.restype = ctypes.c_int
+    lib.rtk_rsthosvd_shard.argtypes = [ctypes.POINTER(_Options), vp, i64p, ctypes.c_int32, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_int32, i32p, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p), vp, vp, ctypes.c_size_t,
+                                       vp, _ALLREDUCE_FN, vp]
+    lib.rtk_rsthosvd_shard.restype = ctypes.c_int
+    lib.rtk_workspace_bytes_shard.argtypes = [ctypes.POINTER(_Options), i64p, ctypes.c_int32, ctypes.c_int64, i32p,
+                                              ctypes.c_int32, ctypes.c_int32]
+    lib.rtk_workspace_bytes_shard.restype = ctypes.c_size_t
     lib.rtk_omega.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                               ctypes.c_int32, vp, vp]
     lib.rtk_omega.restype = ctypes.c_int
@@ -336,3 +349,87 @@ def power_step(M, Q):
         _check(lib.rtk_power_step(ctypes.c_void_p(M.data_ptr()), n, m, ld, ctypes.c_void_p(Qc.data_ptr()),
                                   l, ctypes.c_void_p(Y.data_ptr()), _stream_handle(M.device)))
     return Y.t()
+
+
+class _DeviceBuffer:
+    """A raw device buffer (pointer, count, dtype) seen by torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
+
+
+def shard_bounds(n_last: int, world: int, rank: int):
+    """[begin, begin + count) of mode d held by `rank` when n_last indices are split over `world`
+    ranks as evenly as possible (the first n_last % world ranks hold one more)."""
+    if world < 1 or not 0 <= rank < world or n_last < world:
+        raise ValueError("need 0 <= rank < world <= n_last")
+    base, extra = divmod(int(n_last), int(world))
+    begin = rank * base + min(rank, extra)
+    return begin, base + (1 if rank < extra else 0)
+
+
+def rsthosvd_shard(A_slab, dims, last_begin: int, ranks, p: int, q: int, seed: int, allreduce=None,
+                   root=None, shift: bool = True, omega_kind: int = 0, path: int = 0, out=None, workspace=None):
+    """Alg. 4 on one rank of a group holding A split along its LAST mode (rtk_rsthosvd_shard,
+    SURVEY.md 8(e)): A_slab is this rank's float32 column-major CUDA slab of extents
+    dims[:-1] + [count] covering mode-d indices [last_begin, last_begin + count); dims are the FULL
+    extents.  `allreduce(t)` sums the 1-D CUDA tensor t in place over the group on the current
+    stream (default: torch.distributed.all_reduce on the default group); `root` (default: rank 0 of
+    torch.distributed) is the one rank that applies the shift term -alpha Q before each all-reduce.
+    Returns (core, [U_k]), identical on every rank."""
+    import torch
+    lib = load_library()
+    if not isinstance(A_slab, torch.Tensor) or not A_slab.is_cuda or A_slab.dtype != torch.float32:
+        raise ValueError("A_slab must be a float32 CUDA tensor (no CPU fallback)")
+    if not _is_column_major(A_slab):
+        raise ValueError("A_slab must be column-major (mode-1 fastest); use as_column_major")
+    dims = [int(x) for x in dims]
+    d = len(dims)
+    if A_slab.dim() != d or list(A_slab.shape[:-1]) != dims[:-1]:
+        raise ValueError("A_slab must have extents dims[:-1] + [count]")
+    count = int(A_slab.shape[-1])
+    ranks = [int(r) for r in ranks]
+    if allreduce is None or root is None:
+        import torch.distributed as dist
+        if allreduce is None:
+            def allreduce(t):
+                dist.all_reduce(t)
+        if root is None:
+            root = dist.get_rank() == 0
+    dev = A_slab.device
+    if out is None:
+        U = [torch.empty((r, n), dtype=torch.float32, device=dev).t() for n, r in zip(dims, ranks)]
+        core = as_column_major(torch.empty(ranks, dtype=torch.float32, device=dev))
+    else:
+        core, U = out
+        _check_outputs(core, U, dims, ranks, dev)
+    opt = _Options(1, 1 if shift else 0, 0.0, int(path), 0, int(omega_kind))
+    dd = (ctypes.c_int64 * d)(*dims)
+    rr = (ctypes.c_int32 * d)(*ranks)
+    up = (ctypes.c_void_p * d)(*[u.data_ptr() for u in U])
+    nb = lib.rtk_workspace_bytes_shard(ctypes.byref(opt), dd, d, count, rr, p, q)
+    if nb == 0:
+        raise RtkError(1, lib.rtk_last_error().decode())
+    ws = workspace if workspace is not None else _WS.get(dev, int(nb))
+    errors = []
+
+    def _cb(buf, n, dtype, stream, ctx):
+        try:
+            t = torch.as_tensor(_DeviceBuffer(buf, n, "<f8" if dtype == 1 else "<f4"), device=dev)
+            allreduce(t)
+            return 0
+        except Exception as e:  # noqa: BLE001  (reported below; the C side returns RTK_ERR_CUDA)
+            errors.append(e)
+            return 1
+
+    cb = _ALLREDUCE_FN(_cb)
+    with torch.cuda.device(dev):
+        code = lib.rtk_rsthosvd_shard(ctypes.byref(opt), ctypes.c_void_p(A_slab.data_ptr()), dd, d, int(last_begin),
+                                      count, 1 if root else 0, rr, p, q, ctypes.c_uint64(seed), up,
+                                      ctypes.c_void_p(core.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                      ws.numel() * ws.element_size(), _stream_handle(dev), cb, None)
+    if errors:
+        raise errors[0]
+    _check(code)
+    return core, U

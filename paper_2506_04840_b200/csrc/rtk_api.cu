@@ -109,6 +109,12 @@ struct Problem {
   bool a2 = false;    // Alg. A.2: each mode keeps all l_k columns, then ST-HOSVD of the l-core
   int omega = 0;      // sketch type: 0 RTK-GAUSS-1, 1 uniform, 2 KR-Gaussian, 3 KR-uniform
   std::vector<int> keep;   // columns kept by mode k's shrink: r_k, or l_k = r_k + p (A.2)
+  // multi-GPU last-mode shard: dims[d-1] is this rank's slab, full_last the whole
+  // extent, sh_begin the slab's first index; modes < d-1 all-reduce Y after every streaming pass
+  int64_t full_last = 0, sh_begin = 0;
+  bool sh_root = true;                 // the rank that applies -alpha Q (once) before the all-reduce
+  rtk_allreduce_fn ar = nullptr;
+  void* ar_ctx = nullptr;
 };
 
 void set_keep(Problem& P) {
@@ -121,6 +127,13 @@ std::vector<int64_t> cur_dims(const Problem& P, int k) {
   std::vector<int64_t> e(P.dims);
   if (P.seq)
     for (int j = 0; j < k; ++j) e[j] = P.keep[j];
+  return e;
+}
+
+// the same with the last mode at its full (unsharded) extent: Omega_k's row structure
+std::vector<int64_t> cur_dims_full(const Problem& P, int k) {
+  std::vector<int64_t> e = cur_dims(P, k);
+  if (P.full_last) e[P.d - 1] = P.full_last;
   return e;
 }
 
@@ -310,12 +323,12 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.amax = take((size_t)16 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 16 CTAs
   L.lamx = take((size_t)kSolveLMax * 8);            // eigenvalues shared across the step cluster
-  if (P.omega) {
+  if (P.omega || P.full_last) {   // materialised Omega_k (Appendix D types; every type on a shard)
     size_t oms = 0, tabs = 0;
     for (int k = 0; k < P.d; ++k) {
       const int l = P.ranks[k] + P.p;
       oms = std::max(oms, (size_t)mode_cols(P, k) * l);
-      const std::vector<int64_t> e = cur_dims(P, k);
+      const std::vector<int64_t> e = cur_dims_full(P, k);
       tabs = std::max(tabs, sketch_tab_floats(e.data(), P.d, k + 1, l));
     }
     L.om = take(oms * 4);
@@ -359,7 +372,7 @@ const Layout& plan_cached(const Problem& P, int nsm, const float* A, int path) {
   static thread_local std::vector<std::pair<std::string, Layout>> cache;
   std::string key;
   auto add = [&](long long x) { key += std::to_string(x); key += ','; };
-  add(P.d); add(P.p); add(P.q); add(P.seq); add(P.a2); add(P.omega); add(nsm); add(path);
+  add(P.d); add(P.p); add(P.q); add(P.seq); add(P.a2); add(P.omega); add(nsm); add(path); add(P.full_last);
   add((long long)((uintptr_t)A % 16));
   for (int k = 0; k < P.d; ++k) { add(P.dims[k]); add(P.ranks[k]); add(P.keep[k]); }
   for (const char* ev : {"RTK_PATH", "RTK_PLAN", "RTK_PLAN_SKETCH", "RTK_PLAN_POWER", "RTK_PLAN_SHRINK", "RTK_FUSED",
@@ -443,13 +456,26 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   const bool defer = fast && tc && P.q > 1 && !pve;   // deferred shift updates on the side stream
   if (defer) RTK_CK(side_streams(&side, k));
   bool pending = false;                       // an alpha_kernel is in flight on side->aux
-  const float* om = nullptr;   // Appendix D sketch types: Omega_k materialised once per mode
-  if (P.omega) {
-    const std::vector<int64_t> e = cur_dims(P, k);
+  // a shard's mode k < d-1 factors the column range [j0, j0 + m) of the full unfolding (i_d is the
+  // slowest column index): its partial Y sums to the full one after the all-reduce
+  const bool shard = P.full_last && k < P.d - 1;
+  const float* om = nullptr;   // Appendix D sketch types (and shards): Omega_k materialised once per mode
+  if (P.omega || shard) {
+    const std::vector<int64_t> e = cur_dims_full(P, k);
+    int64_t j0 = 0;
+    if (shard) {
+      int64_t stride = 1;   // column stride of i_d in the mode-k unfolding
+      for (int j = 0; j < P.d - 1; ++j)
+        if (j != k) stride *= e[j];
+      j0 = stride * P.sh_begin;
+    }
     ProfScope ps(0, k, st);
     om = (const float*)(mw + L.om);
-    RTK_CK(sketch_materialize(P.omega, seed, k + 1, e.data(), P.d, 0, v.m(), l, (float*)(mw + L.omtab),
-                              (float*)(mw + L.om), st));
+    if (P.omega)
+      RTK_CK(sketch_materialize(P.omega, seed, k + 1, e.data(), P.d, j0, v.m(), l, (float*)(mw + L.omtab),
+                                (float*)(mw + L.om), st));
+    else
+      RTK_CK(launch_omega(seed, (uint32_t)(k + 1), j0, v.m(), l, (float*)(mw + L.om), st));
     g_launches += 1 + (P.omega >= 2 ? P.d - 1 : 0);
   }
   for (int step = 0; step <= P.q; ++step) {
@@ -509,7 +535,15 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         RTK_CK(cudaStreamWaitEvent(st, side->ev_alpha, 0));
         pending = false;
       }
-      RTK_CK(launch_reduce_gram2(B, step > 0, st, step > 0 ? stop : nullptr));
+      if (shard) {   // Y = sum over ranks of the partial Y (-alpha Q applied once, by the root)
+        RTK_CK(launch_reduce_gram2(B, step > 0 && P.sh_root, st, nullptr, 1));
+        if (P.ar((void*)B.Y, (int64_t)B.n * B.l, 1, (void*)st, P.ar_ctx) != 0)
+          return fail(RTK_ERR_CUDA, "all-reduce callback failed (mode " + std::to_string(k + 1) + ")");
+        RTK_CK(launch_reduce_gram2(B, false, st, nullptr, 2));
+        g_launches += 1;
+      } else {
+        RTK_CK(launch_reduce_gram2(B, step > 0, st, step > 0 ? stop : nullptr));
+      }
       const bool dstep = defer && step > 0 && step < P.q;
       if (dstep) {   // the shift update reads the reduce's Gram partials: it runs beside step_kernel
         RTK_CK(cudaEventRecord(side->ev_step, st));
@@ -729,6 +763,123 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   return RTK_OK;
 }
 
+// ---- multi-GPU last-mode shard -------------------------------------------------
+struct ShardPlan {
+  Problem loc, full;            // the slab (modes < d-1 run on it) and the whole problem (mode d-1)
+  Layout Lloc, Lfull;           // copies: plan_cached's references do not outlive the next insertion
+  size_t gather = 0, total = 0; // offset of the gathered mode-d unfolding, workspace bytes
+  int64_t M = 1, ldf = 0;       // its columns (prod_{j<d-1} r_j) and leading dimension pad4(n_d)
+};
+
+int shard_setup(const rtk_options& o, const float* A, const int64_t* dims, int32_t d, int64_t last_begin,
+                int64_t last_count, const int32_t* ranks, int32_t p, int32_t q, ShardPlan& S) {
+  if (!dims || !ranks) return fail(RTK_ERR_ARG, "NULL pointer argument");
+  if (d < 2 || d > 8) return fail(RTK_ERR_ARG, "d must be in [2, 8]");
+  if (o.sequential != 1 || o.variant != 0 || o.pve_tol > 0.0)
+    return fail(RTK_ERR_ARG, "the last-mode shard runs Alg. 4 (sequential = 1, variant 0, no PVE)");
+  if (o.omega < 0 || o.omega > 3) return fail(RTK_ERR_ARG, "omega must be in [0, 3]");
+  Problem& F = S.full;
+  F.d = d; F.p = p; F.q = q; F.seq = true; F.omega = o.omega;
+  F.dims.assign(dims, dims + d);
+  F.ranks.assign(ranks, ranks + d);
+  set_keep(F);
+  int rc = validate(F);
+  if (rc) return rc;
+  if (last_count < 1 || last_begin < 0 || last_begin + last_count > dims[d - 1])
+    return fail(RTK_ERR_ARG, "the slab [last_begin, last_begin + last_count) must lie inside mode d");
+  for (int k = 0; k + 1 < d; ++k)
+    if (ranks[k] + p > kSolveLMax) return fail(RTK_ERR_ARG, "the shard needs l_k = r_k + p <= 64 for k < d");
+  S.loc = F;
+  S.loc.dims[d - 1] = last_count;
+  S.loc.full_last = dims[d - 1];
+  S.loc.sh_begin = last_begin;
+  S.Lloc = plan_cached(S.loc, num_sms(), A, o.path);
+  S.Lfull = plan_cached(F, num_sms(), A, o.path);
+  S.M = 1;
+  for (int k = 0; k + 1 < d; ++k) S.M *= F.keep[k];
+  S.ldf = pad4(dims[d - 1]);
+  S.gather = align_up(std::max(S.Lloc.total, S.Lfull.total));
+  S.total = S.gather + align_up((size_t)S.ldf * S.M * 4);
+  return RTK_OK;
+}
+
+int solve_shard(const rtk_options& o, const float* A, const int64_t* dims, int32_t d, int64_t last_begin,
+                int64_t last_count, int32_t root, const int32_t* ranks, int32_t p, int32_t q, uint64_t seed,
+                float* const* U, float* core, void* ws_in, size_t ws_bytes, void* stream, rtk_allreduce_fn ar,
+                void* ctx) {
+  if (!A || !U || !core || !ar) return fail(RTK_ERR_ARG, "NULL pointer argument");
+  ShardPlan S;
+  int rc = shard_setup(o, A, dims, d, last_begin, last_count, ranks, p, q, S);
+  if (rc) return rc;
+  for (int k = 0; k < d; ++k)
+    if (!U[k]) return fail(RTK_ERR_ARG, "NULL U[k]");
+  if ((uintptr_t)A % 4) return fail(RTK_ERR_ALIGN, "A must be 4-byte aligned");
+  S.loc.sh_root = root != 0;
+  S.loc.ar = ar;
+  S.loc.ar_ctx = ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  RTK_CK(cudaGetDevice(&dev));
+  int* nflag = numeric_flag_host(dev);
+  if (nflag && *(volatile int*)nflag) {
+    *(volatile int*)nflag = 0;
+    return fail(RTK_ERR_NUMERIC, "an earlier solve on this device hit a numeric failure");
+  }
+  char* ws = (char*)ws_in;
+  bool own = false;
+  if (!ws) {
+    RTK_CK(cudaMallocAsync((void**)&ws, S.total, st));
+    own = true;
+  } else if (ws_bytes < S.total) {
+    return fail(RTK_ERR_WORKSPACE, "workspace too small: need " + std::to_string(S.total) + " bytes");
+  }
+  const Layout& Ll = S.Lloc;
+  const Layout& Lf = S.Lfull;
+  // the report slots sit at the same offsets in both layouts (they depend on d and q only)
+  RTK_CK(cudaMemsetAsync(ws + Lf.status, 0, (size_t)d * 4 * 4, st));
+  RTK_CK(cudaMemsetAsync(ws + Lf.trace, 0, (size_t)d * q * 8, st));
+  const bool shift = o.shift != 0;
+  float* shr[2] = {(float*)(ws + Ll.shr0), (float*)(ws + Ll.shr1)};
+  // modes 1 .. d-1 on the slab; the last shrink leaves the slab's mode-d unfolding in shr[(d-2)&1]
+  for (int k = 0; k + 1 < d; ++k) {
+    const float* cur = k == 0 ? A : shr[(k - 1) & 1];
+    const View rv = range_view(S.loc, k, A, cur);
+    rc = run_mode(S.loc, Ll, ws, k, rv, seed, shift, U[k], st);
+    if (rc) return rc;
+    const View sv = shrink_view(S.loc, k, A, cur);
+    rc = run_shrink(S.loc, Ll, ws, k, sv, U[k], shr[k & 1], st);
+    if (rc) return rc;
+  }
+  // gather: the slab's rows [last_begin, +last_count) of the mode-d unfolding, zero elsewhere, summed
+  float* full = (float*)(ws + S.gather);
+  const float* slab = shr[(d - 2) & 1];
+  RTK_CK(cudaMemsetAsync(full, 0, (size_t)S.ldf * S.M * 4, st));
+  RTK_CK(cudaMemcpy2DAsync(full + last_begin, (size_t)S.ldf * 4, slab, (size_t)pad4(last_count) * 4,
+                           (size_t)last_count * 4, (size_t)S.M, cudaMemcpyDeviceToDevice, st));
+  if (ar((void*)full, (int64_t)S.ldf * S.M, 0, (void*)st, ctx) != 0)
+    return fail(RTK_ERR_CUDA, "all-reduce callback failed (mode-d gather)");
+  // mode d and the core, redundantly on the whole (small) problem
+  {
+    const int k = d - 1;
+    const View rv = range_view(S.full, k, A, full);
+    rc = run_mode(S.full, Lf, ws, k, rv, seed, shift, U[k], st);
+    if (rc) return rc;
+    const View sv = shrink_view(S.full, k, A, full);
+    rc = run_shrink(S.full, Lf, ws, k, sv, U[k], core, st);
+    if (rc) return rc;
+  }
+  if (nflag) {
+    int* dflag = nullptr;
+    RTK_CK(cudaHostGetDevicePointer((void**)&dflag, nflag, 0));
+    numeric_flag_kernel<<<1, 1, 0, st>>>((const int*)(ws + Lf.status), d, dflag);
+    RTK_CK(cudaGetLastError());
+    g_launches += 1;
+  }
+  if (own) RTK_CK(cudaFreeAsync(ws, st));
+  RTK_CK(cudaGetLastError());
+  return RTK_OK;
+}
+
 }  // namespace
 }  // namespace rtk
 
@@ -794,6 +945,29 @@ int rtk_sketch(int32_t kind, uint64_t seed, int32_t mode, const int64_t* dims, i
   RTK_CK(sketch_materialize(kind, seed, mode, dims, d, row0, rows, l, tabs, out, st));
   RTK_CK(cudaFreeAsync(tabs, st));
   return RTK_OK;
+}
+
+int rtk_rsthosvd_shard(const rtk_options* opt, const float* A_slab, const int64_t* dims, int32_t d,
+                       int64_t last_begin, int64_t last_count, int32_t root, const int32_t* ranks, int32_t p,
+                       int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
+                       void* stream, rtk_allreduce_fn allreduce, void* ctx) {
+  rtk_options o = {1, 1, 0.0, 0, 0, 0};
+  if (opt) o = *opt;
+  return rtk::solve_shard(o, A_slab, dims, d, last_begin, last_count, root, ranks, p, q, seed, U, core, ws,
+                          ws_bytes, stream, allreduce, ctx);
+}
+
+size_t rtk_workspace_bytes_shard(const rtk_options* opt, const int64_t* dims, int32_t d, int64_t last_count,
+                                 const int32_t* ranks, int32_t p, int32_t q) {
+  rtk_options o = {1, 1, 0.0, 0, 0, 0};
+  if (opt) o = *opt;
+  rtk::ShardPlan S;
+  if (!dims || d < 2 || d > 8) {
+    g_err = "invalid arguments";
+    return 0;
+  }
+  if (rtk::shard_setup(o, nullptr, dims, d, 0, last_count, ranks, p, q, S)) return 0;
+  return S.total;
 }
 
 size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32_t d, const int32_t* ranks,

@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const long long _tp0 = PCLK();
     for (int64_t s = g; s < total; s += 2) {
       { const long long _t0 = PCLK(); bar_wait_addr(rfull0 + 8u * (uint32_t)sl, rph); PACC(9, _t0); }
+      const long long _tl0 = PCLK();
       float v[kPKS];
 #if RTK_PAIR_PROF || RTK_PAIR_ABL
       if (dbg & 4) {
@@ -577,6 +578,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         lo[e] = d.x; lo[e + 1] = d.y;
       }
       __syncwarp();
+      PACC(12, _tl0);
       if (lane == 0) bar_arrive_addr(rempty0 + 8u * (uint32_t)sl);
       { const long long _t0 = PCLK(); bar_wait_addr(aempty0 + 8u * (uint32_t)ts, tph ^ 1u); PACC(10, _t0); }
       tc_fence_after();
@@ -585,18 +587,24 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       if (!(dbg & 8))
 #endif
       {
+        const long long _t0 = PCLK();
         p_tmem_st64(tq, v, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        PACC(11, _t0);
       }
+      const long long _ta0 = PCLK();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) p_arrive_remote(afull_c0 + 8u * (uint32_t)ts);
+      PACC(13, _ta0);
+      const long long _tw0 = PCLK();
       sl += 2;
       if (sl >= kPRA) { sl -= kPRA; rph ^= 1u; }
       ts += 2;
       if (ts >= SA) { ts -= SA; tph ^= 1u; }
       w.step();
       w.step();
+      PACC(14, _tw0);
     }
     PACC(8, _tp0);
   } else if (warp < 14) {
@@ -872,9 +880,9 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
       for (int r = 0; r < 2; ++r)
         fprintf(stderr,
                 "[pair prof cta%d] mma total %llu wait a_full(op1) %llu q_full %llu a_full(op2) %llu p_full %llu "
-                "w_empty %llu | prod total %llu r_full %llu a_empty %llu st %llu | tma r_empty %llu | epi total %llu "
+                "w_empty %llu | prod total %llu r_full %llu a_empty %llu st %llu lds+split %llu arrive %llu walk %llu | tma r_empty %llu | epi total %llu "
                 "w_full %llu exch %llu p_empty %llu | q q_empty %llu\n",
-                r, h[r][0], h[r][1], h[r][2], h[r][3], h[r][4], h[r][5], h[r][8], h[r][9], h[r][10], h[r][11], h[r][17],
+                r, h[r][0], h[r][1], h[r][2], h[r][3], h[r][4], h[r][5], h[r][8], h[r][9], h[r][10], h[r][11], h[r][12], h[r][13], h[r][14], h[r][17],
                 h[r][20], h[r][21], h[r][22], h[r][23], h[r][24]);
     unsigned long long z[2][32] = {};
     cudaMemcpyToSymbol(g_pair_prof, z, sizeof(z));

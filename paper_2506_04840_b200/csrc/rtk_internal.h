@@ -100,7 +100,10 @@ bool pdl_enabled();   // programmatic dependent launch for the per-step kernels 
 constexpr int kSolveLMax = 64;
 extern double* g_step_dbg;
 size_t solve_gpart_doubles(int n, int l);      // Gram partials of reduce_gram_kernel
-cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop = nullptr);
+// gmode 0: Y = sum of the partials (- alpha Q) and the Gram partials; 1: Y only; 2: the Gram
+// partials of the Y already in B.Y (multi-GPU shards all-reduce Y in between)
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop = nullptr,
+                                int gmode = 0);
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
                         float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st,
                         bool pin_q = false);

@@ -68,7 +68,9 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
                                                          const double* __restrict__ Qd,
                                                          const double* __restrict__ alpha, int power,
                                                          double* __restrict__ Y, double* __restrict__ gpart,
-                                                         const int* __restrict__ stop) {
+                                                         const int* __restrict__ stop, int gmode) {
+  // gmode 0: Y and the Gram partials; 1: Y only (a multi-GPU shard, before Y's all-reduce);
+  // 2: the Gram partials of the (all-reduced) Y already in Y
   __shared__ double Ys[kRBr][kSL + 1];
   __shared__ double red[4][kSL][kRBr];
   __shared__ double gps[kSL * (kSL + 1) / 2];   // this CTA's 8-row Gram (packed upper)
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
   const double a = power ? *alpha : 0.0;
   const int64_t gs = (int64_t)ltot * n_rows;
   static_assert(kRBr == 8 && kST == 4 * kSL, "thread (column c, partial slice h) layout");
-  {   // thread (c, h) sums the partials g = h, h+4, ... of its column's 8 rows: two 16-B loads
+  if (gmode != 2) {   // thread (c, h) sums the partials g = h, h+4, ... of its column's 8 rows: two 16-B loads
       // per partial, all independent (the rows past n are Ypart padding, masked below; n_rows is a
       // multiple of 4, and a last group with only 4 rows inside n_rows takes the scalar loop)
     const int c = tid % kSL, h = tid / kSL;
@@ -126,12 +128,17 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
     double s = 0.0;
     if (ii < rows) {   // the four slices in a fixed order: repeatable results
       const int i = i0 + ii;
-      s = ((red[0][c][ii] + red[1][c][ii]) + red[2][c][ii]) + red[3][c][ii];
-      if (power) s -= a * Qd[(int64_t)c * n + i];
-      Y[(int64_t)c * n + i] = s;
+      if (gmode == 2) {
+        s = Y[(int64_t)c * n + i];
+      } else {
+        s = ((red[0][c][ii] + red[1][c][ii]) + red[2][c][ii]) + red[3][c][ii];
+        if (power) s -= a * Qd[(int64_t)c * n + i];
+        Y[(int64_t)c * n + i] = s;
+      }
     }
     Ys[ii][c] = s;
   }
+  if (gmode == 1) return;   // uniform over the grid: before any cluster barrier
   __syncthreads();
   const int np = l * (l + 1) / 2;
   for (int e = tid; e < np; e += kST) {
@@ -1761,7 +1768,7 @@ int solve_cluster_size(int n) {
 
 size_t solve_gpart_doubles(int n, int l) { return (size_t)gram_blocks(n) * l * (l + 1) / 2; }
 
-cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop) {
+cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop, int gmode) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(gram_blocks(B.n) * kRGC, 1, 1);   // CTAs past n contribute zero rows
   cfg.blockDim = dim3(kST, 1, 1);
@@ -1777,7 +1784,7 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, reduce_gram_kernel, (const float*)B.Ypart, B.G, B.ltot, B.n_rows, B.n,
                                      B.l, (const double*)B.Qd, (const double*)B.alpha, power ? 1 : 0, B.Y, B.gpart,
-                                     stop);
+                                     stop, gmode);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
