@@ -413,6 +413,75 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_shard(args, ws, rank, local):
+    """--shard: ONE C5 solve per step with A split along its last mode over the ws ranks
+    (rtk_rsthosvd_shard): each GPU holds and streams 1/ws of the tensor, an NCCL
+    all-reduce sums the n_k x l panel Y after every streaming pass, the small solves and mode d run
+    redundantly.  Strong scaling: value = max-over-ranks ms per (whole-problem) solve."""
+    import torch
+
+    from paper_2506_04840_b200 import build as b
+    if rank == 0:
+        b.build()
+    barrier(ws)
+    import paper_2506_04840_b200 as rt
+    from workloads import CONFIGS, make_config_tensor_torch
+
+    c = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dims = list(c["dims"])
+    begin, count = rt.shard_bounds(dims[-1], ws, rank)
+    A = make_config_tensor_torch(args.config, device=dev)
+    S = rt.as_column_major(A[..., begin:begin + count])
+    del A
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    ranks, p, q, seed = c["ranks"], c["p"], c["q"], c["omega_seed"]
+    if ws > 1:
+        import torch.distributed as dist
+
+        def allreduce(t):
+            dist.all_reduce(t)
+    else:
+        def allreduce(t):
+            return None
+    U = [torch.empty((r, n), dtype=torch.float32, device=dev).t() for n, r in zip(dims, ranks)]
+    core = rt.as_column_major(torch.empty(ranks, dtype=torch.float32, device=dev))
+
+    def step():
+        rt.rsthosvd_shard(S, dims, begin, ranks, p, q, seed, allreduce=allreduce, root=rank == 0, out=(core, U))
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream(dev)
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = clk.stop()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms_step, "unit": "ms", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32 stream / f64 small solves",
+                "data": "synthetic", "config": cfg_block(args.config, c),
+                "parallelism": f"last-mode shard x{ws}: n_{len(dims)} = {dims[-1]} split into slabs of "
+                               f"{dims[-1] // ws}-{-(-dims[-1] // ws)} per GPU, one n_k x l fp64 all-reduce per "
+                               "streaming pass (NCCL), mode d redundant",
+                "roofline": None, "cpu_baseline": None, "e2e": None, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -422,6 +491,8 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one solve per step with A split along its last mode over the GPUs (strong scaling)")
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="reference arm: stop timing further oracle solves after this many seconds")
     args = ap.parse_args()
@@ -431,7 +502,10 @@ def main():
         run_reference(args, ws, rank)
         return
     ws, rank, local = dist_init(args)
-    run_ours(args, ws, rank, local)
+    if args.shard:
+        run_shard(args, ws, rank, local)
+    else:
+        run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
