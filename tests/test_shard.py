@@ -148,7 +148,7 @@ def test_sharded_alg4_gloo_world_size_2_equals_oracle():
 
 
 # ---------------------------------------------------------------------------------------- GPU
-def _gpu_worker(rank, world, port, dims, ranks, p, q, out):
+def _gpu_worker(rank, world, port, dims, ranks, p, q, out, kind=0):
     import torch
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
@@ -167,8 +167,8 @@ def _gpu_worker(rank, world, port, dims, ranks, p, q, out):
     b, c = rt.shard_bounds(dims[-1], world, rank)
     A = to_device_colmajor(a, torch)
     S = to_device_colmajor(np.ascontiguousarray(a[..., b:b + c]), torch)
-    core1, u1 = rt.rsthosvd(A, ranks, p, q, 19)
-    core_s, u_s = rt.rsthosvd_shard(S, dims, b, ranks, p, q, 19)
+    core1, u1 = rt.rsthosvd(A, ranks, p, q, 19, omega_kind=kind)
+    core_s, u_s = rt.rsthosvd_shard(S, dims, b, ranks, p, q, 19, omega_kind=kind)
     torch.cuda.synchronize()
     c0, cs = core1.double().cpu().numpy(), core_s.double().cpu().numpy()
     out[rank] = (float(np.abs(cs - c0).max() / np.abs(c0).max()),
@@ -199,5 +199,32 @@ def test_shard_matches_single_gpu(dims, ranks, p, q):
         assert pr.exitcode == 0
     assert out[0][2] == out[1][2]            # identical outputs on both ranks
     for r in range(2):
+        dcore, du, _, _ = out[r]
+        assert dcore <= 2e-5 and du <= 2e-4, (r, dcore, du)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,kind", [(3, 0), (2, 2), (2, 1)])
+def test_shard_world3_and_sketch_types(world, kind):
+    """Three ranks (slabs 7 / 7 / 6 of n_3 = 20) with the Gaussian sketch, and two ranks with the
+    Khatri-Rao Gaussian and the uniform sketch (Omega_k's rows for the slab's column range, with the
+    Khatri-Rao factor of mode d drawn over its full extent)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    dims, ranks, p, q = (300, 40, 20), (20, 8, 5), 6, 2
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, dims, ranks, p, q, out, kind))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(600)
+        assert pr.exitcode == 0
+    for r in range(world):
+        assert out[r][2] == out[0][2]
         dcore, du, _, _ = out[r]
         assert dcore <= 2e-5 and du <= 2e-4, (r, dcore, du)
