@@ -313,7 +313,7 @@ __device__ __noinline__ bool chol_upper(const double* A, double* R, double* flag
 // T has leading dimension kMLD.  (Measured in the step kernel: 28k cycles against 39k for a 4 x 4
 // block-diagonal sweep; a recursive 8 -> 64 block version was no faster there.)
 __device__ __noinline__ void tri_inv_upper(const double* R, double* T, int l, double* rinv) {
-  (void)l;   // R is the identity beyond l, so is T
+  // R is the identity beyond l, so is T; for l <= 32 the off-diagonal products vanish
   const int tid = threadIdx.x;
   constexpr int H = kSL / 2;
   static_assert(kST >= 4 * H && kST % H == 0, "thread layout");
@@ -342,6 +342,14 @@ __device__ __noinline__ void tri_inv_upper(const double* R, double* T, int l, do
     for (int i = 0; i < H; ++i) T[(lo + i) * kMLD + lo + lane] = t[i];
   }
   __syncthreads();
+  if (l <= H) {   // R12 = 0 and R22 = I (R is the identity beyond l): T12 = 0, T22 = I (done above)
+    for (int idx = tid; idx < H * H; idx += kST) {
+      T[(idx / H) * kMLD + H + idx % H] = 0.0;
+      T[(H + idx / H) * kMLD + idx % H] = 0.0;
+    }
+    __syncthreads();
+    return;
+  }
   // X = R12 T22 (rows i < H, columns c >= H) staged in the lower-left block: X(i, c) at T(H + i, c - H)
   const int cc = tid % H, g = tid / H, rows = H / (kST / H);   // thread: column H + cc, rows g*rows ..
   {
