@@ -776,9 +776,13 @@ bool pair_supported(const View& v, int l) {
   // default for n_k > 256 (C3 / C5 mode 1): each CTA streams all rows of its 128 columns, which halves
   // the B-operand and Q traffic per SM; for n_k <= 256 the one-CTA engine's 128-row tiles waste less
   // (a pair-tile is 256 rows).  RTK_PAIR=0 / 1 forces it off / on.
+  // and for unfoldings with at least one 256-column pair-block per two pairs: narrower ones (C5 mode
+  // 3, m = 2500: 10 pair-blocks) are faster on the one-CTA engine's 128-column blocks (ncu, 1000 x
+  // 2500: 27 vs 36 us; 1000 x 5e4: 99 vs 88 us -- scripts/ncu_small_m.sh; in the solve C3 mode 2,
+  // 47 pair-blocks, stays faster on the pair)
   const char* e = getenv("RTK_PAIR");
   if (e && e[0] == '0') return false;
-  if (!(e && e[0] == '1') && v.n <= 256) return false;
+  if (!(e && e[0] == '1') && (v.n <= 256 || (v.m() + kPBJ - 1) / kPBJ < num_sms() / 4)) return false;
   const int N = tc_npad(l);
   if (!N) return false;
   if (!(v.P == 1 && v.si == 1 && v.ss >= v.n && v.ss % 4 == 0 && ((uintptr_t)v.base % 16) == 0)) return false;

@@ -1246,6 +1246,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
       }
     }
     __syncthreads();
+    if (i0 == r0) tck[ntck++] = clock64();
     if (eig && S.flags[1]) {
       // rank-deficient columns (flagged invalid): deterministic Philox completion, which the
       // second CholQR pass orthonormalises against the valid ones

@@ -129,6 +129,8 @@ def test_fused_sketch_engine(seq, dims, ranks, p, q, engine, monkeypatch):
     (RTK_PAIR_SKETCH=0): oracle parity incl. alpha traces."""
     monkeypatch.setenv("RTK_FUSED_SKETCH_MIN", "0")
     monkeypatch.setenv("RTK_PAIR_SKETCH", "1" if engine == "pair" else "0")
+    if engine == "pair":
+        monkeypatch.setenv("RTK_PAIR", "1")   # these unfoldings have fewer pair-blocks than pairs
     rng = np.random.default_rng(sum(dims) + 101)
     cr = tuple(min(n, r + 3) for n, r in zip(dims, ranks))
     core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
@@ -150,6 +152,7 @@ def test_pair_shrink_engine(dims, ranks, monkeypatch):
     core = rng.standard_normal(cr) * np.exp(-0.25 * np.indices(cr).sum(axis=0))
     a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
     monkeypatch.setenv("RTK_PAIR_SHRINK", "1")
+    monkeypatch.setenv("RTK_PAIR", "1")   # m_1 = 7290 / 4810: fewer pair-blocks than pairs otherwise
     check(a, ranks, 6, 2, 31, True, ew_cols=0)
     A = to_device_colmajor(a, torch)
     core1, u1 = solve(A, ranks, 6, 2, 31, sequential=True)
