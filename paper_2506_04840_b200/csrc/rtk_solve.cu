@@ -955,8 +955,9 @@ __device__ void stage_rows(const double* X, int n, int l, int i0, int nr, double
   __syncthreads();
 }
 
-// Q rows [i0, i0+nr) staged in Xs -> fp64 master, fp32 shadow and (if planes) the 3xTF32 B
-// planes of the next op1 (hi = round-to-nearest tf32, lo = exact remainder), rows fastest.
+// Q rows [i0, i0+nr) staged in Xs -> fp64 master and either the 3xTF32 B planes of the next op1
+// (hi = round-to-nearest tf32, lo = exact remainder; the tcgen05 paths) or the fp32 shadow the FFMA
+// tiles read, rows fastest.
 __device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, double* Qd, float* Qs,
                               float* planes, int pN, int pld) {
   const int cols = planes ? pN : l;
@@ -968,7 +969,7 @@ __device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, do
       const float f = (float)v;
       if (c < l) {
         Qd[o] = v;
-        Qs[o] = f;
+        if (!planes) Qs[o] = f;
       }
       if (planes) {
         const float hi = sm100::tf32_rna(f);
