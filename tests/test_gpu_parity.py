@@ -442,11 +442,16 @@ def test_a2_rejected_where_undefined():
 # ------------------------------------------------------------ Appendix D sketch types
 @pytest.mark.parametrize("kind", [1, 2, 3])
 @pytest.mark.parametrize("algo", ["t", "st", "a2"])
-@pytest.mark.parametrize("path", ["ffma", "fused"])
+@pytest.mark.parametrize("path", ["ffma", "fused", "pair"])
 def test_sketch_type_parity(kind, algo, path, monkeypatch):
-    """Uniform / KR-Gaussian / KR-uniform sketches through every algorithm and streaming path."""
+    """Uniform / KR-Gaussian / KR-uniform sketches through every algorithm and streaming path
+    (pair: the CTA-pair engine forced for every contiguous mode, its sketch fed by the materialised
+    Omega's planes)."""
     monkeypatch.setenv("RTK_PATH", "ffma" if path == "ffma" else "tc")
-    monkeypatch.setenv("RTK_FUSED", "1" if path == "fused" else "0")
+    monkeypatch.setenv("RTK_FUSED", "0" if path == "ffma" else "1")
+    if path == "pair":
+        monkeypatch.setenv("RTK_PAIR", "1")
+        monkeypatch.setenv("RTK_FUSED_SKETCH_MIN", "0")
     torch = cuda_or_skip()
     from paper_2506_04840_b200 import solve
     rng = np.random.default_rng(60 + kind)
