@@ -98,6 +98,7 @@ constexpr int kNMax = 4096;
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 int64_t pad4(int64_t n) { return (n + 3) / 4 * 4; }
+int64_t pad8(int64_t n) { return (n + 7) / 8 * 8; }
 
 struct Problem {
   int d = 0;
@@ -220,6 +221,7 @@ struct Layout {
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
   size_t g2part = 0, gsum = 0, amax = 0, lamx = 0;
+  size_t xmax = 0;   // [8] floats: max|M| of each mode's unfolding (the fp16 pair engine's scale)
   size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
   size_t om = 0, omtab = 0;                                         // Appendix D sketches only
   size_t mode_size = 0;   // bytes of one mode's scratch region (T-HOSVD: one region per mode)
@@ -293,6 +295,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.trace = take((size_t)P.d * P.q * 8);
   L.sigma = take((size_t)P.d * 128 * 8);
   L.status = take((size_t)P.d * 4 * 4);
+  L.xmax = take(8 * 4);
   L.shr0 = take(shr * 4);
   L.shr1 = take(shr * 4);
   if (P.a2) {
@@ -419,8 +422,20 @@ cudaError_t mode_streams(ModeStreams** out) {
   } while (0)
 
 // Alg. 3/4 lines 3-12 for one mode (mode index k, 0-based); writes U_k.
+// max|M| bookkeeping for the fp16 pair power step (rtk_fused2.cu): xmax[k] holds max|M| of mode k's
+// unfolding once a pair sketch of mode k or the pair shrink of mode k-1 has written it (ready[k]).
+struct XState {
+  float* xmax = nullptr;
+  char ready[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+static bool pair_f16_enabled() {
+  const char* e = getenv("RTK_PAIR_F16");
+  return !(e && e[0] == '0');
+}
+
 int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, uint64_t seed,
-             bool shift, float* Uk, cudaStream_t st) {
+             bool shift, float* Uk, cudaStream_t st, XState* xs = nullptr) {
   const int n = v.n, r = P.ranks[k], l = r + P.p;
   char* mw = ws + (P.seq ? 0 : (size_t)k * L.mode_size);   // this mode's scratch region
   ModeBufs B;
@@ -478,6 +493,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       RTK_CK(launch_omega(seed, (uint32_t)(k + 1), j0, v.m(), l, (float*)(mw + L.om), st));
     g_launches += 1 + (P.omega >= 2 ? P.d - 1 : 0);
   }
+  // the power steps run on the fp16 pair engine when max|M| of this unfolding is known (decided
+  // after the sketch, which may provide it)
+  const bool h16c = xs && fast && fused && pair_supported(v, l) && pair_f16_enabled();
+  bool h16 = false;
   for (int step = 0; step <= P.q; ++step) {
     const TilePlan& tp = step == 0 ? L.sk[k] : L.pw[k];
     if (tc) {
@@ -490,9 +509,15 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       if (fused && (step > 0 || strided || v.m() >= fused_sketch_min())) {   // sketch: Omega planes in the W buffer (ld = ldw >= m)
         int Gf = 0, rows = 0;
         const bool sk = step == 0;
-        RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (int)pad4(n), sk, seed, mode1, B.Ypart,
-                           pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st, nullptr, 1, 1,
-                           1, sk ? nullptr : stop, om));
+        PairScale ps;
+        if (h16c) {
+          if (sk) ps.xmax_out = xs->xmax + k;
+          else ps.xmax_in = h16 ? xs->xmax + k : nullptr;
+        }
+        RTK_CK(fused_power(v, l, sk ? W : planes, sk ? (int)L.ldw : (h16 ? (int)pad8(n) : (int)pad4(n)), sk, seed,
+                           mode1, B.Ypart, pending ? num_sms() - fused_cluster(n) : num_sms(), &Gf, &rows, st,
+                           nullptr, 1, 1, 1, sk ? nullptr : stop, om, &ps));
+        if (ps.wrote) xs->ready[k] = 1;
         g_launches += (sk && !fused_sketch_gen(om)) ? 1 : 0;   // omega_planes_kernel
         g_launches += 1;
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
@@ -528,6 +553,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
     }
     B.G = tp.G; B.ltot = tp.ltot(); B.n_rows = tp.n_rows();
     }
+    if (step == 0) h16 = h16c && xs->ready[k];   // the planes the step kernels write from here on
     if (fast) {
       ProfScope ps(3, k, st);
       float* planes = tc ? (float*)(mw + L.planes) : nullptr;
@@ -557,7 +583,8 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
       // A.2: the pinned fp32 basis replaces the shadow Qs (the shrink's matrix), Qd pinned in place
       float* uout = P.a2 ? (float*)(mw + L.qs) : Uk;
       RTK_CK(launch_step(B, step, P.q, shift, (step == P.q || (pve && step > 0)) ? uout : nullptr, seed, mode1,
-                         planes, tc_npad(l), (int)pad4(n), dstep, pve ? P.pve : 0.0, st, P.a2));
+                         planes, tc_npad(l), h16 ? (int)pad8(n) : (int)pad4(n), dstep, pve ? P.pve : 0.0, st, P.a2,
+                         h16));
       g_launches += 2;
     } else {
       ProfScope ps(3, k, st);
@@ -578,7 +605,7 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
 
 // G x_k U_k^T written as the next unfolding (or the canonical core after mode d).
 int run_shrink(const Problem& P, const Layout& L, char* ws, int k, const View& v, const float* Uk, float* out,
-               cudaStream_t st) {
+               cudaStream_t st, XState* xs = nullptr) {
   TileLaunch T;
   T.v = v;
   T.op = OP_SHRINK;
@@ -599,8 +626,11 @@ int run_shrink(const Problem& P, const Layout& L, char* ws, int k, const View& v
     float* planes = (float*)(ws + L.planes);
     RTK_CK(tc_split(nullptr, Uk, v.n, kk, planes, st));
     int Gf = 0, rows = 0;
+    PairScale ps;   // the pair shrink records max|M| of the next unfolding it writes
+    if (xs && k + 1 < P.d && pair_f16_enabled()) ps.xmax_out = xs->xmax + k + 1;
     RTK_CK(fused_power(v, kk, planes, (int)pad4(v.n), false, 0, 0, nullptr, num_sms(), &Gf, &rows, st, out,
-                       T.Rprev, T.nnext, T.ldnext));
+                       T.Rprev, T.nnext, T.ldnext, nullptr, nullptr, &ps));
+    if (ps.wrote) xs->ready[k + 1] = 1;
     g_launches += 2;
     return RTK_OK;
   }
@@ -670,6 +700,9 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
   }
   RTK_CK(cudaMemsetAsync(ws + L.status, 0, (size_t)d * 4 * 4, st));
   RTK_CK(cudaMemsetAsync(ws + L.trace, 0, (size_t)d * q * 8, st));
+  RTK_CK(cudaMemsetAsync(ws + L.xmax, 0, 8 * 4, st));
+  XState xst;
+  xst.xmax = (float*)(ws + L.xmax);
   float* shr[2] = {(float*)(ws + L.shr0), (float*)(ws + L.shr1)};
   const bool shift = opt.shift != 0;
   if (P.a2) {
@@ -680,13 +713,14 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
     for (int k = 0; k < d; ++k) {
       const float* cur = k == 0 ? A : shr[(k - 1) & 1];
       const View rv = range_view(P, k, A, cur);
-      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st, &xst);
       if (rc) return rc;
       qk[k] = (double*)(ws + L.a2q) + qoff;
       qoff += (size_t)P.dims[k] * P.keep[k];
       RTK_CK(cudaMemcpyAsync(qk[k], ws + L.qd, (size_t)P.dims[k] * P.keep[k] * 8, cudaMemcpyDeviceToDevice, st));
       const View sv = shrink_view(P, k, A, cur);
-      rc = run_shrink(P, L, ws, k, sv, (const float*)(ws + L.qs), k + 1 < d ? shr[k & 1] : (float*)(ws + L.a2b), st);
+      rc = run_shrink(P, L, ws, k, sv, (const float*)(ws + L.qs), k + 1 < d ? shr[k & 1] : (float*)(ws + L.a2b), st,
+                      &xst);
       if (rc) return rc;
     }
     {   // lines 14-15: ST-HOSVD of the l_1 x ... x l_d tensor, U_k = Q_k V_k
@@ -701,10 +735,10 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
     for (int k = 0; k < d; ++k) {
       const float* cur = k == 0 ? A : shr[(k - 1) & 1];
       const View rv = range_view(P, k, A, cur);
-      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], st, &xst);
       if (rc) return rc;
       const View sv = shrink_view(P, k, A, cur);
-      rc = run_shrink(P, L, ws, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st);
+      rc = run_shrink(P, L, ws, k, sv, U[k], k + 1 < d ? shr[k & 1] : core, st, &xst);
       if (rc) return rc;
     }
   } else {
@@ -716,7 +750,7 @@ int solve(const rtk_options& opt, const float* A, const int64_t* dims, int32_t d
     for (int k = 0; k < d; ++k) {
       RTK_CK(cudaStreamWaitEvent(ms->s[k], ms->fork, 0));
       const View rv = range_view(P, k, A, nullptr);
-      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], ms->s[k]);
+      rc = run_mode(P, L, ws, k, rv, seed, shift, U[k], ms->s[k], &xst);
       if (rc) return rc;
       RTK_CK(cudaEventRecord(ms->join[k], ms->s[k]));
     }
@@ -1009,16 +1043,29 @@ int rtk_power_step(const float* M, int64_t n, int64_t m, int64_t ld, const float
   if (!(pe && std::string(pe) == "ffma") && tc_supported(v, l) && !(fz && fz[0] == '0') && fused_supported(v, l)) {
     // the fused single-pass engine of the solver (rtk_fused.cu)
     const int N = tc_npad(l), G = num_sms();
-    const int64_t pld = pad4(n);
-    float *planes = nullptr, *yp = nullptr;
+    // RTK_POWER_F16=1 (test hook only): the fp16 pair engine, with max|M| and the fp16 Q planes
+    // prepared here the way the solver's sketch / shrink and step kernels prepare them
+    const char* pf = getenv("RTK_POWER_F16");
+    const bool h16 = pf && pf[0] == '1' && pair_supported(v, l);
+    const int64_t pld = h16 ? pad8(n) : pad4(n);
+    float *planes = nullptr, *yp = nullptr, *xm = nullptr;
     RTK_CK(cudaMallocAsync((void**)&planes, (size_t)2 * N * pld * 4, st));
     RTK_CK(cudaMallocAsync((void**)&yp, fused_ypart_floats(v, l, G) * 4, st));
-    RTK_CK(tc_split(nullptr, Q, (int)n, l, planes, st));
+    PairScale ps;
+    if (h16) {
+      RTK_CK(cudaMallocAsync((void**)&xm, 4, st));
+      RTK_CK(pair_prepare16(v, Q, l, N, (int)pld, planes, xm, st));
+      ps.xmax_in = xm;
+    } else {
+      RTK_CK(tc_split(nullptr, Q, (int)n, l, planes, st));
+    }
     int Gf = 0, rows = 0;
-    RTK_CK(fused_power(v, l, planes, (int)pld, false, 0, 0, yp, G, &Gf, &rows, st));
+    RTK_CK(fused_power(v, l, planes, (int)pld, false, 0, 0, yp, G, &Gf, &rows, st, nullptr, 1, 1, 1, nullptr,
+                       nullptr, &ps));
     RTK_CK(launch_sum_partials(yp, Gf, N, rows, (int)n, l, Y, st));
     RTK_CK(cudaFreeAsync(planes, st));
     RTK_CK(cudaFreeAsync(yp, st));
+    if (xm) RTK_CK(cudaFreeAsync(xm, st));
     return RTK_OK;
   }
   if (!(pe && std::string(pe) == "ffma") && tc_supported(v, l)) {

@@ -28,6 +28,7 @@
 // (W -> exchange -> op2 B planes; final Y), 14 TMA Q half-planes.
 // Y partials go to Ypart[pair][c][row] (row pitch nt * 256) for the fixed-order fp64 reduction.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,7 +49,7 @@ constexpr int kPRA = 6;         // A tile ring slots (16 KB each)
 constexpr int kPRQ = 6;         // Q half-plane ring slots
 constexpr int kPTile = 128 * 32 * 4;
 constexpr int kPBJ = 256;       // columns per pair-block
-constexpr int kPK2 = kPBJ / kPKS;   // op2 stages per pair-tile (8)
+constexpr int kPRAH = 4;        // A ring slots of the fp16 engine (32 KB each)
 
 // Role timers (-DRTK_PAIR_PROF=1 builds only; clock reads cost issue slots): summed wait / busy
 // cycles of the two CTAs of pair 0, printed by the host at the next launch.
@@ -91,6 +92,11 @@ struct PairArgs {
   int lk;          // shrink: output columns (r_k <= N)
   int sketch;      // 1: the sketch Y = M Omega -- op2 only, B = the Omega planes streamed through the
                    // Q ring one 32-column K chunk at a time (K chunk outer, pair-tile inner), no W
+  // fp16 two-plane power step (H = true, see pair_power_kernel): max|M| of this unfolding (device),
+  // and cW = ceil(log2 sqrt(n)) for the W scale
+  const float* xmax_in;
+  int cW;
+  float* xmax_out; // tf32 sketch / shrink: atomicMax of max|M| (sketch) or of the written entries (shrink)
 };
 
 // Stage order shared by the TMA, MMA and producer warps ("lagged" order):
@@ -213,9 +219,18 @@ __device__ __forceinline__ uint32_t p_elect_one() {
                : "+r"(pred));
   return pred;
 }
-template <uint32_t IDESC>
+template <uint32_t IDESC, bool H>
 __device__ __forceinline__ void p_mma3(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t bhi, uint64_t blo,
                                        uint32_t acc) {
+  if constexpr (H) {   // fp16 planes (A from TMEM: two fp16 per 32-bit column), same operand walk
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%2], %3, %6, p;\n"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], [%1], %4, %6, 1;\n"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], [%1], %3, %6, 1;\n}\n" ::"r"(d),
+        "r"(ahi), "r"(alo), "l"(bhi), "l"(blo), "r"(acc), "n"(IDESC));
+    return;
+  }
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n"
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %6, p;\n"
@@ -226,26 +241,6 @@ __device__ __forceinline__ void p_mma3(uint32_t d, uint32_t ahi, uint32_t alo, u
 __device__ __forceinline__ void p_commit_one(uint64_t* b) {   // elected lane only
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_addr(b)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-// the three 3xTF32 products of one K-step on the pair: D (+)= A_lo B_hi + A_hi B_lo + A_hi B_hi
-template <uint32_t IDESC>
-__device__ __forceinline__ void p_umma3(uint32_t d, uint32_t ahi, uint32_t alo, uint64_t bhi, uint64_t blo,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %5, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%2], %3, %6, p;\n"
-      "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], [%1], %4, %6, 1;\n"
-      "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], [%1], %3, %6, 1;\n}\n" ::"r"(d),
-      "r"(ahi), "r"(alo), "l"(bhi), "l"(blo), "r"(acc), "n"(IDESC));
-}
-// arrive (once) on the same-offset mbarrier of both CTAs when this thread's MMAs complete
-__device__ __forceinline__ void p_commit_mc(uint64_t* b) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
           smem_addr(b)),
       "h"((uint16_t)3)
       : "memory");
@@ -299,41 +294,80 @@ __device__ __forceinline__ void p_tmem_st64(uint32_t taddr, const float (&v)[32]
       "f"(w[28]), "f"(w[29]), "f"(w[30]), "f"(w[31])
       : "memory");
 }
-__device__ __forceinline__ void p_tmem_st32(uint32_t taddr, const float (&v)[32]) {
+__device__ __forceinline__ void p_tmem_st64u(uint32_t taddr, const uint32_t (&v)[32], const uint32_t (&w)[32]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
-      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
-      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,"
+      "%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]),
+      "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+      "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
       : "memory");
+}
+// warp max of v (>= 0), one atomicMax per warp on the float's bits (monotone for v >= 0)
+__device__ __forceinline__ void p_atomic_max(float* dst, float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(dst), __float_as_uint(v));
+}
+// eA with max|M| 2^eA in [2^14, 2^15) (the fp16 engine's scale of M), clamped so that 2^eA and the
+// Y factor stay normal floats
+__device__ __forceinline__ int p_scale_exp(const float* xmax) {
+  const float am = *xmax;
+  const int e = (am > 0.f && am <= 3.4e38f) ? ilogbf(am) : 0;
+  return max(-113, min(126, 14 - e));
 }
 
 }  // namespace
 
 // SA: TMEM A stages (2: W double-buffered; 3: W single-buffered -- safe with this stage order,
 // where op1(jb+1) follows op2(jb-1), long after W(jb) was drained -- and one more stage in flight)
-template <int N, int SA>
+//
+// H = true: the power step with fp16 two-plane operands ("3xFP16") instead of 3xTF32.  Each operand
+// x is scaled by a power of two s and split x s = h + l, h = fp16_rn(x s), l = fp16_rn(x s - h): 11 + 11
+// significand bits, the same 22 bits a tf32 hi/lo pair carries, and the three products h h', h l',
+// l h' are exact in the fp32 accumulator, so the result has the 3xTF32 error.  The
+// fp16 exponent range is handled by the scales: M by 2^eA with max|M| 2^eA in [2^14, 2^15) (max|M| from
+// the sketch / shrink pass that produced the unfolding), Q by 2^15 (|q| <= 1, the step kernel's
+// planes), W = M^T Q by 2^-(15 + cW) (|W_jc| <= ||M_j|| ||Q_c|| <= sqrt(n) max|M|, Cauchy-Schwarz);
+// every scale is exact and Y is multiplied back by 2^(cW - 2 eA) when it leaves TMEM.  Entries far
+// below the maximum lose relative (not absolute) precision to fp16 gradual underflow: absolute error
+// <= 2^-25 of the scaled unit, ~2^-40 of max|M| (2^-35 after the W bound).  A stage is 64 K (the
+// fp16 MMA takes K = 16 per instruction in the same 32 bytes), so every per-stage handshake covers
+// twice the data, and the TMEM A stage (hi 32 + lo 32 columns of packed pairs) keeps its size.
+template <int N, int SA, bool H>
 __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                                   const __grid_constant__ CUtensorMap tmA,
                                                                   const __grid_constant__ CUtensorMap tmA2,
                                                                   const PairArgs a) {
   constexpr int N2 = N / 2;                  // B rows held by each CTA
-  constexpr int QS = 2 * N2 * 128;           // Q ring slot: hi | lo half-planes of 32 rows
-  constexpr int PL = (kPBJ / 32) * N2 * 128; // one op2 B plane: 256 columns x N2
-  constexpr uint32_t IDESC = idesc_tf32(256, N, 0, 0);
+  constexpr int KS = H ? 64 : kPKS;          // K per stage
+  constexpr int SLOT = H ? 2 * kPTile : kPTile;   // A ring slot: one stage (H: two 32-K TMA boxes)
+  constexpr int NRA = H ? kPRAH : kPRA;      // A ring slots
+  constexpr int K2 = kPBJ / KS;              // op2 stages per pair-tile
+  constexpr int QS = 2 * N2 * 128;           // Q ring slot: hi | lo half-planes of one stage (128-B rows)
+  constexpr int PL = K2 * N2 * 128;          // one op2 B plane: 256 columns x N2
+  constexpr uint32_t IDESC = H ? idesc_f16(256, N) : idesc_tf32(256, N, 0, 0);
   constexpr int NW = SA == 2 ? 2 : 1;         // W buffers
   constexpr int TA0 = 256 + NW * N;          // TMEM: Y tiles at 0, W buffers at 256, A ring
   static_assert(N % 16 == 0 && N >= 16 && N <= 64, "cta_group::2 N");
-  static_assert(TA0 + 2 * kPKS * SA <= 512, "TMEM budget");
+  static_assert(TA0 + 64 * SA <= 512, "TMEM budget");
+  // the two producer groups take alternate stages and must own disjoint ring slots / TMEM stages
+  // (a slot shared by both groups lets one group's parity wait pass on the other group's older
+  // phase), so both ring depths are even
+  static_assert(NRA % 2 == 0 && SA % 2 == 0 || SA == 3, "ring depth vs producer groups");
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = smraw + ((1024u - (smem_addr(smraw) & 1023u)) & 1023u);
-  uint8_t* smR = sm;                          // kPRA x kPTile
-  uint8_t* smQ = smR + kPRA * kPTile;         // kPRQ x QS
+  uint8_t* smR = sm;                          // NRA x SLOT
+  uint8_t* smQ = smR + NRA * SLOT;            // kPRQ x QS
   uint8_t* smP = smQ + kPRQ * QS;             // hi plane | lo plane
   float* rbuf = (float*)(smP + 2 * PL);       // 128 x N2 received from the peer
-  __shared__ __align__(8) uint64_t r_full[kPRA], r_empty[kPRA], q_full[kPRQ], q_empty[kPRQ];
+  __shared__ __align__(8) uint64_t r_full[NRA], r_empty[NRA], q_full[kPRQ], q_empty[kPRQ];
   __shared__ __align__(8) uint64_t a_full[SA], a_empty[SA], w_full[2], w_empty[2];
   __shared__ __align__(8) uint64_t p_full, p_empty, y_full, x_full, credit;
   __shared__ uint32_t tbase_s;
@@ -348,14 +382,14 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   const bool leader = rank == 0;
   const int64_t pid = blockIdx.x >> 1, P = gridDim.x >> 1;
   const int64_t nb = (a.nblk > pid) ? (a.nblk - pid + P - 1) / P : 0;   // pair-blocks of this pair
-  const int nk1 = SKT ? 0 : a.nk1, nk2 = a.nt * kPK2;
+  const int nk1 = SKT ? 0 : a.nk1, nk2 = a.nt * K2;
   const int lagL = a.lag < 0 ? 0 : (a.lag > nk1 ? nk1 : a.lag);   // op1(b+1) stages ahead of op2(b)
   const int64_t total = nb * (nk1 + nk2);
 
   // stage order (TMA, MMA and producer warps alike): op1(0), [op1(1)], op2(0), op1(2), op2(1), ..., op2(nb-1)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kPRA; ++s) { bar_init(&r_full[s], 1); bar_init(&r_empty[s], 4); }
+    for (int s = 0; s < NRA; ++s) { bar_init(&r_full[s], 1); bar_init(&r_empty[s], 4); }
     for (int s = 0; s < kPRQ; ++s) { bar_init(&q_full[s], 1); bar_init(&q_empty[s], 1); }
     for (int s = 0; s < SA; ++s) { bar_init(&a_full[s], 8); bar_init(&a_empty[s], 1); }
     for (int b = 0; b < 2; ++b) { bar_init(&w_full[b], 1); bar_init(&w_empty[b], 8); }
@@ -389,29 +423,34 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       uint32_t ph = 0;
       auto load = [&](int op, int x, int64_t y) {
         { const long long _t0 = PCLK(); bar_wait(&r_empty[sl], ph ^ 1); PACC(17, _t0); }
-        uint8_t* dst = smR + sl * kPTile;
+        uint8_t* dst = smR + sl * SLOT;
         if (dbg & 2) {
           bar_arrive(&r_full[sl]);
         } else {
-          bar_expect_tx(&r_full[sl], kPTile);
-          if (op == 1) p_tma_load(dst, &tmA, x, (int)y, &r_full[sl], SHR ? pol_drop : pol_keep);   // [128 j][32 i], SW128
-          else p_tma_load(dst, &tmA2, x, (int)y, &r_full[sl], pol_drop);         // [32 c][128 i]
+          bar_expect_tx(&r_full[sl], SLOT);
+          if (op == 1) {   // [128 j][32 i], SW128 (H: rows x.. and x + 32.. as two such tiles)
+            p_tma_load(dst, &tmA, x, (int)y, &r_full[sl], SHR ? pol_drop : pol_keep);
+            if constexpr (H) p_tma_load(dst + kPTile, &tmA, x + 32, (int)y, &r_full[sl], pol_keep);
+          } else {         // [32 c][128 i] (H: [64 c][128 i])
+            p_tma_load(dst, &tmA2, x, (int)y, &r_full[sl], pol_drop);
+            if constexpr (H) p_tma_load(dst + kPTile, &tmA2, x, (int)y + 32, &r_full[sl], pol_drop);
+          }
         }
-        if (++sl == kPRA) { sl = 0; ph ^= 1; }
+        if (++sl == NRA) { sl = 0; ph ^= 1; }
       };
       const int L = lagL;
       auto seg1 = [&](int64_t blk, int k0, int k1) {   // all rows of this CTA's 128 columns
         const int64_t y = colbase(blk) + 128 * rank;
-        for (int k = k0; k < k1; ++k) load(1, kPKS * k, y);
+        for (int k = k0; k < k1; ++k) load(1, KS * k, y);
       };
       auto seg2 = [&](int64_t blk) {                    // this CTA's rows of each pair-tile x 256 columns
         const int64_t c0 = colbase(blk);
         if (SKT) {   // the MMA's sketch order: K chunk outer, pair-tile inner
-          for (int kq = 0; kq < kPK2; ++kq)
-            for (int tt = 0; tt < a.nt; ++tt) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+          for (int kq = 0; kq < K2; ++kq)
+            for (int tt = 0; tt < a.nt; ++tt) load(2, 256 * tt + 128 * (int)rank, c0 + KS * kq);
         } else {
           for (int tt = 0; tt < a.nt; ++tt)
-            for (int kq = 0; kq < kPK2; ++kq) load(2, 256 * tt + 128 * (int)rank, c0 + kPKS * kq);
+            for (int kq = 0; kq < K2; ++kq) load(2, 256 * tt + 128 * (int)rank, c0 + KS * kq);
         }
       };
       if (nb > 0) seg1(0, 0, L);
@@ -444,11 +483,11 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         if (p_elect_one()) {
           const uint32_t d = 256u + (uint32_t)(b * N);
           const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
-          const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+          const uint32_t ta = (uint32_t)(TA0 + 64 * sa);
           if (mma_on) {
 #pragma unroll
             for (int k8 = 0; k8 < 4; ++k8)
-              p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+              p_mma3<IDESC, H>(d, ta + 8 * k8, ta + 32 + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
                             qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (k | k8) != 0);
           }
           p_commit_one(&a_empty[sa]);
@@ -464,16 +503,16 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         for (int t = 0; t < a.nt; ++t) {
           const uint32_t d = (uint32_t)(t * N);
 #pragma unroll 1
-          for (int kq = 0; kq < kPK2; ++kq) {
+          for (int kq = 0; kq < K2; ++kq) {
             { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
             tc_fence_after();
             if (p_elect_one()) {
-              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+              const uint32_t ta = (uint32_t)(TA0 + 64 * sa);
               if (mma_on) {
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8) {
                   const uint32_t boff = (uint32_t)(kq * (N2 * 128) + k8 * 32);
-                  p_mma3<IDESC>(d, ta + 8 * k8, ta + kPKS + 8 * k8, p0 + (uint64_t)(boff >> 4),
+                  p_mma3<IDESC, H>(d, ta + 8 * k8, ta + 32 + 8 * k8, p0 + (uint64_t)(boff >> 4),
                                 p0 + (uint64_t)((PL + boff) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
                 }
               }
@@ -488,7 +527,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       };
       auto op2s = [&](int64_t blk) {          // sketch op2(blk): K chunk kq (Omega, Q ring) x pair-tile t
 #pragma unroll 1
-        for (int kq = 0; kq < kPK2; ++kq) {
+        for (int kq = 0; kq < K2; ++kq) {
           { const long long _t0 = PCLK(); bar_wait(&q_full[qsl], qph); PACC(2, _t0); }
           const uint64_t qs = q0 + (uint64_t)((qsl * QS) >> 4);
 #pragma unroll 1
@@ -496,11 +535,11 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
             { const long long _t0 = PCLK(); bar_wait(&a_full[sa], aph); PACC(3, _t0); }
             tc_fence_after();
             if (p_elect_one()) {
-              const uint32_t ta = (uint32_t)(TA0 + 2 * kPKS * sa);
+              const uint32_t ta = (uint32_t)(TA0 + 64 * sa);
               if (mma_on) {
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8)
-                  p_mma3<IDESC>((uint32_t)(t * N), ta + 8 * k8, ta + kPKS + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
+                  p_mma3<IDESC, H>((uint32_t)(t * N), ta + 8 * k8, ta + 32 + 8 * k8, qs + (uint64_t)((k8 * 32) >> 4),
                                 qs + (uint64_t)((N2 * 128 + k8 * 32) >> 4), (blk > 0 || kq > 0 || k8 > 0) ? 1u : 0u);
               }
               p_commit_one(&a_empty[sa]);
@@ -548,11 +587,43 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     if (g == 1) w.step();
     int sl = g, ts = g;                            // ring slot / TMEM stage of this group's stage
     uint32_t rph = 0, tph = 0;
+    float vmax = 0.f;                              // sketch: running max|M|
+    float sA = 1.f;                                // H: the exact scale 2^eA of M
+    if constexpr (H) sA = ldexpf(1.f, p_scale_exp(a.xmax_in));
     const long long _tp0 = PCLK();
     for (int64_t s = g; s < total; s += 2) {
       { const long long _t0 = PCLK(); bar_wait_addr(rfull0 + 8u * (uint32_t)sl, rph); PACC(9, _t0); }
       const long long _tl0 = PCLK();
-      float v[kPKS];
+      float v[kPKS], lo[kPKS];          // tf32: hi (the raw value) and lo planes
+      uint32_t hv[32], lv[32];          // H: packed fp16 pairs (k, k + 1) of the hi and lo planes
+      if constexpr (H) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {   // the stage's two 32-K halves
+          float x[32];
+          if (w.op == 1) {
+            const uint32_t base = tile1 + (uint32_t)sl * SLOT + (uint32_t)(hf * kPTile);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 y = lds128(base + ((((uint32_t)c) ^ sw) << 4));
+              x[4 * c] = y.x; x[4 * c + 1] = y.y; x[4 * c + 2] = y.z; x[4 * c + 3] = y.w;
+            }
+          } else {
+            const uint32_t base = tile2 + (uint32_t)sl * SLOT + (uint32_t)(hf * kPTile);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[c] = lds32(base + (uint32_t)(c * 512));
+          }
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 xs = __fmul2_rn(make_float2(x[e], x[e + 1]), make_float2(sA, sA));   // exact
+            const __half2 h = __floats2half2_rn(xs.x, xs.y);
+            const float2 hb = __half22float2(h);
+            const float2 r = __fadd2_rn(xs, make_float2(-hb.x, -hb.y));                      // exact
+            const __half2 l2 = __floats2half2_rn(r.x, r.y);
+            hv[16 * hf + e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+            lv[16 * hf + e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+          }
+        }
+      } else {
 #if RTK_PAIR_PROF || RTK_PAIR_ABL
       if (dbg & 4) {
 #pragma unroll
@@ -560,35 +631,40 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       } else
 #endif
       if (w.op == 1) {
-        const uint32_t base = tile1 + (uint32_t)sl * kPTile;
+        const uint32_t base = tile1 + (uint32_t)sl * SLOT;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 x = lds128(base + ((((uint32_t)c) ^ sw) << 4));
           v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
         }
       } else {
-        const uint32_t base = tile2 + (uint32_t)sl * kPTile;
+        const uint32_t base = tile2 + (uint32_t)sl * SLOT;
 #pragma unroll
         for (int c = 0; c < kPKS; ++c) v[c] = lds32(base + (uint32_t)(c * 512));
+        if (SKT) {   // max|M| of the unfolding (every element passes through one sketch stage)
+#pragma unroll
+          for (int c = 0; c < kPKS; ++c) vmax = fmaxf(vmax, fabsf(v[c]));
+        }
       }
-      float lo[kPKS];
 #pragma unroll
       for (int e = 0; e < kPKS; e += 2) {
         const float2 d = __fadd2_rn(make_float2(v[e], v[e + 1]), make_float2(-tf32_trunc(v[e]), -tf32_trunc(v[e + 1])));
         lo[e] = d.x; lo[e + 1] = d.y;
+      }
       }
       __syncwarp();
       PACC(12, _tl0);
       if (lane == 0) bar_arrive_addr(rempty0 + 8u * (uint32_t)sl);
       { const long long _t0 = PCLK(); bar_wait_addr(aempty0 + 8u * (uint32_t)ts, tph ^ 1u); PACC(10, _t0); }
       tc_fence_after();
-      const uint32_t tq = tq0 + (uint32_t)(2 * kPKS * ts);
+      const uint32_t tq = tq0 + (uint32_t)(64 * ts);
 #if RTK_PAIR_PROF || RTK_PAIR_ABL
       if (!(dbg & 8))
 #endif
       {
         const long long _t0 = PCLK();
-        p_tmem_st64(tq, v, lo);
+        if constexpr (H) p_tmem_st64u(tq, hv, lv);
+        else p_tmem_st64(tq, v, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         PACC(11, _t0);
       }
@@ -599,7 +675,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       PACC(13, _ta0);
       const long long _tw0 = PCLK();
       sl += 2;
-      if (sl >= kPRA) { sl -= kPRA; rph ^= 1u; }
+      if (sl >= NRA) { sl -= NRA; rph ^= 1u; }
       ts += 2;
       if (ts >= SA) { ts -= SA; tph ^= 1u; }
       w.step();
@@ -607,6 +683,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       PACC(14, _tw0);
     }
     PACC(8, _tp0);
+    if (SKT && a.xmax_out) p_atomic_max(a.xmax_out, vmax);
   } else if (warp < 14) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;
@@ -616,6 +693,14 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     const uint32_t rdst = p_mapa(smem_addr(rbuf + j * N2), peer);
     const uint32_t rbar = p_mapa(smem_addr(&x_full), peer);
     const uint32_t rcredit = p_mapa(smem_addr(&credit), peer);
+    float emax = 0.f;   // shrink: running max of the entries written
+    float tW = 1.f;     // H: the exact scale 2^-(15 + cW) of W
+    double yback = 1.0; // H: Y = TMEM value * 2^(cW - 2 eA)
+    if constexpr (H) {
+      const int eA = p_scale_exp(a.xmax_in);
+      tW = ldexpf(1.f, -(15 + a.cW));
+      yback = ldexp(1.0, a.cW - 2 * eA);
+    }
     const long long _te0 = PCLK();
     for (int64_t jb = 0; jb < (SKT ? 0 : nb); ++jb) {
       const int b = NW == 2 ? (int)(jb & 1) : 0;
@@ -643,7 +728,10 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
           float* o = a.out + bb + a.ldnext * (aa + a.Rprev * (int64_t)a.lk * cc);
 #pragma unroll
           for (int c = 0; c < N; ++c)
-            if (c < a.lk) o[cs * c] = w[c];
+            if (c < a.lk) {
+              o[cs * c] = w[c];
+              emax = fmaxf(emax, fabsf(w[c]));
+            }
           if (bb == a.nnext - 1 && a.ldnext > a.nnext)   // zero the row padding of this column
             for (int cr = 0; cr < a.lk; ++cr)
               for (int64_t z = 1; z < a.ldnext - a.nnext + 1; ++z) o[cs * cr + z] = 0.f;
@@ -683,6 +771,21 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       // column at 128 peer + j; hi = rna tf32, lo exact; once op2(jb-1) has released the planes
       { const long long _t0 = PCLK(); p_wait_sleep(&p_empty, (uint32_t)((jb & 1) ^ 1)); PACC(23, _t0); }
       const int ko = 128 * (int)rank + j, kp = 128 * (int)peer + j;
+      if constexpr (H) {   // fp16 planes [K/64][N2 c][64 k] (128-B rows, SW128), W scaled by tW
+        const uint32_t ro = (uint32_t)((ko >> 6) * (N2 * 128) + (((ko & 63) >> 3) << 4) + ((ko & 7) << 1));
+        const uint32_t rp = (uint32_t)((kp >> 6) * (N2 * 128) + (((kp & 63) >> 3) << 4) + ((kp & 7) << 1));
+#pragma unroll
+        for (int c = 0; c < N2; ++c) {
+          const float xo = wo[c] * tW, xp = pw[c] * tW;
+          const __half ho = __float2half_rn(xo), hp = __float2half_rn(xp);
+          const __half lo2 = __float2half_rn(xo - __half2float(ho)), lp2 = __float2half_rn(xp - __half2float(hp));
+          const uint32_t sw16 = (uint32_t)((c & 7) << 4), rb = (uint32_t)(c * 128);
+          *reinterpret_cast<__half*>(smP + ((ro ^ sw16) + rb)) = ho;
+          *reinterpret_cast<__half*>(smP + PL + ((ro ^ sw16) + rb)) = lo2;
+          *reinterpret_cast<__half*>(smP + ((rp ^ sw16) + rb)) = hp;
+          *reinterpret_cast<__half*>(smP + PL + ((rp ^ sw16) + rb)) = lp2;
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < N2; ++c) {
         const float xo = wo[c], xp = pw[c];
@@ -694,11 +797,13 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
         *reinterpret_cast<float*>(smP + op) = hp;
         *reinterpret_cast<float*>(smP + PL + op) = xp - hp;
       }
+      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) p_arrive_cluster(pfull_c);
     }
     PACC(20, _te0);
+    if (SHR && a.xmax_out) p_atomic_max(a.xmax_out, emax);
     // ---- final: this CTA's Y rows (its half of every pair-tile) -> Ypart[pair][c][row]
     const int rows_tot = a.nt * 256;
     float* yp = a.Ypart + pid * (int64_t)N * rows_tot;
@@ -717,7 +822,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
           for (int c = 0; c < 16; ++c) v[c] = 0.f;
         }
 #pragma unroll
-        for (int c = 0; c < 16; ++c) yp[(int64_t)(c0 + c) * rows_tot + i] = v[c];
+        for (int c = 0; c < 16; ++c) yp[(int64_t)(c0 + c) * rows_tot + i] = H ? (float)((double)v[c] * yback) : v[c];
       }
     }
     tc_fence_before();
@@ -731,13 +836,13 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     uint32_t ph = 0;
     // sketch: the K chunks of the Omega planes (columns colbase + 32 kq of the pair-block), read once
     const uint64_t pol_q = SKT ? p_policy_first() : pol_keep;
-    const int nq = SKT ? kPK2 : nk1;
+    const int nq = SKT ? K2 : nk1;
     for (int64_t jb = 0; jb < nb; ++jb)
       for (int k = 0; k < nq; ++k) {
         { const long long _t0 = PCLK(); bar_wait(&q_empty[sl], ph ^ 1); PACC(24, _t0); }
         uint8_t* sq = smQ + sl * QS;
         const uint32_t cb = qfull0 + 8u * (uint32_t)sl;
-        const int x = SKT ? (int)(colbase(jb) + kPKS * k) : kPKS * k;
+        const int x = SKT ? (int)(colbase(jb) + KS * k) : KS * k;
         if (dbg & 16) {
           if (leader) bar_arrive(&q_full[sl]);
         } else {
@@ -751,6 +856,32 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
   __syncthreads();
   p_cluster_sync();   // no CTA releases TMEM / leaves while the peer may still use it
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+// ---------------------------------------------------------------------- test hook helpers
+__global__ void absmax_kernel(const float* __restrict__ M, int n, int64_t m, int64_t ld, float* xmax) {
+  float v = 0.f;
+  for (int64_t j = blockIdx.x; j < m; j += gridDim.x)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v = fmaxf(v, fabsf(M[j * ld + i]));
+  p_atomic_max(xmax, v);
+}
+__global__ void split16_kernel(const float* __restrict__ Q, int n, int l, int N, int pld, __half* planes) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)N * pld;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / pld), i = (int)(idx % pld);
+    const double x = (c < l && i < n) ? (double)Q[(int64_t)c * n + i] * 32768.0 : 0.0;
+    const __half hi = __float2half_rn((float)x);
+    planes[(int64_t)c * pld + i] = hi;
+    planes[(int64_t)(N + c) * pld + i] = __float2half_rn((float)(x - (double)__half2float(hi)));
+  }
+}
+cudaError_t pair_prepare16(const View& v, const float* Q, int l, int N, int pld, float* planes, float* xmax,
+                           cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(xmax, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  absmax_kernel<<<1024, 256, 0, st>>>(v.base, v.n, v.m(), v.ss, xmax);
+  split16_kernel<<<256, 256, 0, st>>>(Q, v.n, l, N, pld, reinterpret_cast<__half*>(planes));
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------- host side
@@ -795,12 +926,12 @@ size_t pair_ypart_floats(const View& v, int l, int grid) {
   return (size_t)(grid / 2) * N * nt * 256;
 }
 
-template <int N, int SA>
+template <int N, int SA, bool H>
 static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, const CUtensorMap& ta2, const PairArgs& a,
                                int grid, cudaStream_t st) {
-  const size_t smem = 1024 + (size_t)kPRA * kPTile + (size_t)kPRQ * 2 * (N / 2) * 128 +
-                      2 * (size_t)(kPBJ / 32) * (N / 2) * 128 + (size_t)128 * (N / 2) * 4;
-  cudaError_t e = cudaFuncSetAttribute(pair_power_kernel<N, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = 1024 + (size_t)(H ? kPRAH * 2 * kPTile : kPRA * kPTile) + (size_t)kPRQ * 2 * (N / 2) * 128 +
+                      2 * (size_t)(kPBJ / (H ? 64 : 32)) * (N / 2) * 128 + (size_t)128 * (N / 2) * 4;
+  cudaError_t e = cudaFuncSetAttribute(pair_power_kernel<N, SA, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -816,7 +947,7 @@ static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, con
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  e = cudaLaunchKernelEx(&cfg, pair_power_kernel<N, SA>, tq, ta, ta2, a);
+  e = cudaLaunchKernelEx(&cfg, pair_power_kernel<N, SA, H>, tq, ta, ta2, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -825,22 +956,30 @@ static cudaError_t pair_launch(const CUtensorMap& tq, const CUtensorMap& ta, con
 // Ypart[grid/2][N][nt*256]; returns the partial count and row pitch.
 cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
                        int* rows_out, cudaStream_t st, const int* stop, float* shrink_out, int64_t Rprev,
-                       int64_t nnext, int64_t ldnext, bool sketch) {
+                       int64_t nnext, int64_t ldnext, bool sketch, PairScale* ps) {
+  // the fp16 two-plane power step: planes are fp16 [2N][pld] (pld a multiple of 8), scaled by 2^15
+  const bool H = ps && ps->xmax_in && !sketch && !shrink_out;
+  const int KS = H ? 64 : kPKS;
   const int N = tc_npad(l), nt = shrink_out ? 0 : (v.n + 255) / 256;
   const int64_t m = v.m();
   const int64_t nblk = (m + kPBJ - 1) / kPBJ;
   int pairs = std::max(1, grid / 2);
   pairs = (int)std::min<int64_t>(pairs, std::max<int64_t>(1, nblk));   // no idle pairs (zero partials)
   PairArgs a;
-  a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + kPKS - 1) / kPKS; a.nblk = nblk;
+  a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + KS - 1) / KS; a.nblk = nblk;
   a.Ypart = Ypart; a.stop = stop;
-  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : 8;
+  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : (H ? 4 : 8);   // stages (H: 64 rows each)
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
   a.shrink = shrink_out ? 1 : 0;
   a.out = shrink_out;
   a.Rprev = Rprev; a.nnext = nnext; a.ldnext = ldnext;
   a.lk = l;
   a.sketch = sketch ? 1 : 0;
+  a.xmax_in = H ? ps->xmax_in : nullptr;
+  a.xmax_out = (ps && (sketch || shrink_out)) ? ps->xmax_out : nullptr;
+  if (a.xmax_out) ps->wrote = true;
+  a.cW = 0;
+  while ((1ll << (2 * a.cW)) < (long long)v.n) ++a.cW;   // ceil(log2 sqrt(n))
   CUtensorMap tq, ta, ta2;
   memset(&tq, 0, sizeof(tq));
   memset(&ta, 0, sizeof(ta));
@@ -865,11 +1004,14 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
       return cudaErrorInvalidValue;
   }
   {   // Q planes [2N][pld]: box {32 rows i, N/2 columns c}, SWIZZLE_128B ([N/2 c][32 i]); the sketch's
-      // Omega planes [2N][pld >= m] the same way with the unfolding's columns j in place of i
+      // Omega planes [2N][pld >= m] the same way with the unfolding's columns j in place of i.
+      // H: fp16 planes, box {64 rows i, N/2 columns c} (128-B rows as well)
     cuuint64_t dims[2] = {(cuuint64_t)(sketch ? m : v.n), (cuuint64_t)(2 * N)};
-    cuuint64_t strides[1] = {(cuuint64_t)pld * 4};
-    cuuint32_t box[2] = {32, (cuuint32_t)(N / 2)};
-    if (pair_encode_fn()(&tq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(planes), dims, strides, box, es,
+    cuuint64_t strides[1] = {(cuuint64_t)pld * (H ? 2 : 4)};
+    cuuint32_t box[2] = {(cuuint32_t)(H ? 64 : 32), (cuuint32_t)(N / 2)};
+    if (H && (pld % 8)) return cudaErrorInvalidValue;
+    if (pair_encode_fn()(&tq, H ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<float*>(planes), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
@@ -894,11 +1036,19 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
 #endif
   const char* se = getenv("RTK_PAIR_SA");
   const bool sa3 = se && se[0] == '3';   // SA = 3 needs op1(b) to start after W(b-1) was drained
+  if (H) {
+    switch (N) {
+      case 16: return pair_launch<16, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
+      case 32: return pair_launch<32, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
+      case 48: return pair_launch<48, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
+      default: return pair_launch<64, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
+    }
+  }
   switch (N) {
-    case 16: return sa3 ? pair_launch<16, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<16, 2>(tq, ta, ta2, a, 2 * pairs, st);
-    case 32: return sa3 ? pair_launch<32, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<32, 2>(tq, ta, ta2, a, 2 * pairs, st);
-    case 48: return sa3 ? pair_launch<48, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<48, 2>(tq, ta, ta2, a, 2 * pairs, st);
-    default: return sa3 ? pair_launch<64, 3>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<64, 2>(tq, ta, ta2, a, 2 * pairs, st);
+    case 16: return sa3 ? pair_launch<16, 3, false>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<16, 2, false>(tq, ta, ta2, a, 2 * pairs, st);
+    case 32: return sa3 ? pair_launch<32, 3, false>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<32, 2, false>(tq, ta, ta2, a, 2 * pairs, st);
+    case 48: return sa3 ? pair_launch<48, 3, false>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<48, 2, false>(tq, ta, ta2, a, 2 * pairs, st);
+    default: return sa3 ? pair_launch<64, 3, false>(tq, ta, ta2, a, 2 * pairs, st) : pair_launch<64, 2, false>(tq, ta, ta2, a, 2 * pairs, st);
   }
 }
 

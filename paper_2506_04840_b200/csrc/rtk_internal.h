@@ -106,7 +106,7 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
                                 int gmode = 0);
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
                         float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st,
-                        bool pin_q = false);
+                        bool pin_q = false, bool planes16 = false);
 cudaError_t launch_alpha(const ModeBufs& B, int step, bool shift, cudaStream_t st);
 // Alg. A.2 lines 14-15 (rtk_solve.cu): deterministic ST-HOSVD of the l_1 x ... x l_d fp32 tensor B
 // and U_k = Q_k V_k (sign-pinned); g0/g1 hold prod(l) doubles each, gram/V 64*64 doubles.
@@ -123,6 +123,16 @@ cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t 
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
                    float* Ypart, int G, cudaStream_t st, const float* om = nullptr);
 
+// The fp16 two-plane power step and its scale (rtk_fused2.cu): xmax_in = max|M| of the
+// unfolding (device) selects it for a power step (planes are then fp16 [2N][pld], pld % 8 == 0, scaled
+// by 2^15); xmax_out receives (atomicMax) max|M| from a pair sketch, or the max of the entries a pair
+// shrink writes (the next unfolding's max|M|).
+struct PairScale {
+  const float* xmax_in = nullptr;
+  float* xmax_out = nullptr;
+  bool wrote = false;   // set by pair_power when its launch writes xmax_out
+};
+
 // ---- fused single-pass power step (rtk_fused.cu) -----------------------------------
 int fused_cluster(int n);
 bool fused_sketch_gen(const float* om);   // fused sketch generates Omega in-kernel (no planes kernel)
@@ -131,7 +141,7 @@ size_t fused_ypart_floats(const View& v, int l, int grid);
 cudaError_t fused_power(const View& v, int l, const float* planes, int pld, bool sketch, uint64_t seed,
                         uint32_t mode1, float* Ypart, int grid, int* G_out, int* rows_out, cudaStream_t st,
                         float* shrink_out = nullptr, int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1,
-                        const int* stop = nullptr, const float* om = nullptr);
+                        const int* stop = nullptr, const float* om = nullptr, PairScale* ps = nullptr);
 
 // ---- fused power step on a CTA pair, tcgen05 cta_group::2 (rtk_fused2.cu) ---------------
 bool pair_supported(const View& v, int l);
@@ -139,9 +149,14 @@ size_t pair_ypart_floats(const View& v, int l, int grid);
 // shrink_out != nullptr: the mode shrink G x_k U_k^T instead (op1 only, planes = U's, l = r_k),
 // written as the next unfolding (Rprev, nnext, ldnext as in TileLaunch).  sketch: Y = M Omega_k
 // (op2 only) with planes = the Omega planes [2N][pld >= m] of omega_planes_kernel.
+// test hook support (rtk_power_step with RTK_POWER_F16=1): max|M| into xmax and the fp16 planes of
+// the fp32 Q (n x l, column-major) as the step kernel writes them (2^15 q = hi + lo)
+cudaError_t pair_prepare16(const View& v, const float* Q, int l, int N, int pld, float* planes, float* xmax,
+                           cudaStream_t st);
 cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float* Ypart, int grid, int* G_out,
                        int* rows_out, cudaStream_t st, const int* stop, float* shrink_out = nullptr,
-                       int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1, bool sketch = false);
+                       int64_t Rprev = 1, int64_t nnext = 1, int64_t ldnext = 1, bool sketch = false,
+                       PairScale* ps = nullptr);
 
 // ---- Appendix D sketch types (rtk_omega.cu) ------------------------------------------
 // Materialise Omega_k rows [row0, row0 + rows) x l (row-major [j][l]) of the given type for the

@@ -154,6 +154,12 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor, kind::f16 with fp16 A and B (a_format = b_format = F16 = 0), fp32 accumulate,
+// both operands K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // fp32 -> tf32 round-to-nearest (value kept in an fp32 container, low 13 bits zero)
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;

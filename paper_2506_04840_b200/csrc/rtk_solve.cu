@@ -27,6 +27,7 @@
 // runs are bit-identical.  Cross-CTA data goes through global memory (L2) ordered by
 // barrier.cluster (release/acquire), read with ld.global.cg.
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -878,6 +879,7 @@ struct StepArgs {
   float* Qs;                // [l][n]
   float* planes;            // [2 pN][pld] 3xTF32 planes of Q for the next op1 (nullptr: none)
   int pN, pld;
+  int planes16;             // planes are the fp16 engine's: __half [2 pN][pld], Q scaled by 2^15
   double* alpha;
   double* trace;            // [q]
   double* sigma;            // [128]
@@ -959,7 +961,7 @@ __device__ void stage_rows(const double* X, int n, int l, int i0, int nr, double
 // (hi = round-to-nearest tf32, lo = exact remainder; the tcgen05 paths) or the fp32 shadow the FFMA
 // tiles read, rows fastest.
 __device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, double* Qd, float* Qs,
-                              float* planes, int pN, int pld) {
+                              float* planes, int pN, int pld, int p16) {
   const int cols = planes ? pN : l;
   for (int idx = threadIdx.x; idx < cols * kChunk; idx += kST) {
     const int c = idx / kChunk, row = idx % kChunk;
@@ -971,7 +973,13 @@ __device__ void write_outputs(const double* Xs, int nr, int i0, int n, int l, do
         Qd[o] = v;
         if (!planes) Qs[o] = f;
       }
-      if (planes) {
+      if (planes && p16) {   // fp16 engine (rtk_fused2.cu): 2^15 q = hi + lo, |q| <= 1
+        const double x = v * 32768.0;
+        const __half hi = __float2half_rn((float)x);
+        const __half lo = __float2half_rn((float)(x - (double)__half2float(hi)));
+        reinterpret_cast<__half*>(planes)[(int64_t)c * pld + i0 + row] = hi;
+        reinterpret_cast<__half*>(planes)[(int64_t)(pN + c) * pld + i0 + row] = lo;
+      } else if (planes) {
         const float hi = sm100::tf32_rna(f);
         planes[(int64_t)c * pld + i0 + row] = hi;
         planes[(int64_t)(pN + c) * pld + i0 + row] = (float)(v - (double)hi);
@@ -1269,7 +1277,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
         if (row < nr) a.Q1[(int64_t)c * n + i0 + row] = Xs[row * kLD + c];
       }
     } else {
-      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld);
+      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld, a.planes16);
     }
     if (two_pass) {
       // Gram2 partial (upper 4 x 4 blocks) of the Q1 rows now in Xs
@@ -1329,7 +1337,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
         }
       }
       __syncthreads();
-      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld);
+      write_outputs(Xs, nr, i0, n, l, a.Qd, a.Qs, a.planes, a.pN, a.pld, a.planes16);
       __syncthreads();
     }
   }
@@ -1345,7 +1353,8 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   if (a.planes && rank == C - 1) {
     for (int idx = tid; idx < 2 * a.pN * (a.pld - n); idx += kST) {
       const int c = idx / (a.pld - n), i = n + idx % (a.pld - n);
-      a.planes[(int64_t)c * a.pld + i] = 0.f;
+      if (a.planes16) reinterpret_cast<__half*>(a.planes)[(int64_t)c * a.pld + i] = __float2half_rn(0.f);
+      else a.planes[(int64_t)c * a.pld + i] = 0.f;
     }
   }
 
@@ -1801,13 +1810,13 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
 
 cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U, uint64_t seed, uint32_t mode1,
                         float* planes, int pN, int pld, bool defer_alpha, double pve_tol, cudaStream_t st,
-                        bool pin_q) {
+                        bool pin_q, bool planes16) {
   StepArgs a;
   a.n = B.n; a.l = B.l; a.r = B.r; a.step = step; a.q = q;
   a.shift = shift ? 1 : 0; a.final_step = (step == q) ? 1 : 0;
   a.nblk = gram_blocks(B.n);
   a.gpart = B.gpart; a.Y = B.Y; a.Q1 = B.Q1; a.g2part = B.g2part; a.gsum = B.gsum; a.amax = B.amax;
-  a.Qd = B.Qd; a.Qs = B.Qs; a.planes = planes; a.pN = pN; a.pld = pld;
+  a.Qd = B.Qd; a.Qs = B.Qs; a.planes = planes; a.pN = pN; a.pld = pld; a.planes16 = planes16 ? 1 : 0;
   a.alpha = B.alpha; a.trace = B.trace; a.sigma = B.sigma; a.status = B.status;
   a.U = U; a.seed = seed; a.mode1 = mode1;
   a.dbg = g_step_dbg;

@@ -80,6 +80,40 @@ def test_power_step_vs_fp64(n, m, l, path, monkeypatch):
     assert ew < TOL_EW[path], ew
 
 
+# The fp16 two-plane pair engine (rtk_fused2.cu, H = true): the same 22-bit split as
+# 3xTF32, so the same bounds.  Forced onto the pair engine (RTK_PAIR=1) at every shape; `scale`
+# multiplies M (exponent range: the power-of-two scales must follow max|M|), `spread` gives the
+# columns of M magnitudes over 2^-spread .. 1 (fp16 gradual underflow of the small entries).
+@pytest.mark.parametrize("n,m,l,scale,spread", [
+    (3, 50, 2, 1.0, 0), (64, 4096, 10, 1.0, 0), (200, 3000, 30, 1.0, 0), (400, 2001, 40, 1.0, 0),
+    (1000, 1234, 60, 1.0, 0), (37, 333, 13, 1.0, 0), (130, 5000, 64, 1.0, 0), (1000, 200000, 60, 1.0, 0),
+    (256, 129, 48, 1.0, 0), (513, 777, 17, 1.0, 0), (600, 3000, 48, 1.0, 0), (1024, 4099, 33, 1.0, 0),
+    (1000, 40000, 60, 1e-15, 0), (1000, 40000, 60, 1e15, 0), (700, 9000, 24, 3e-3, 20),
+    (1000, 20000, 60, 1.0, 40)])
+def test_power_step_f16_pair_vs_fp64(n, m, l, scale, spread, monkeypatch):
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import power_step
+    monkeypatch.setenv("RTK_PATH", "tc")
+    monkeypatch.setenv("RTK_FUSED", "1")
+    monkeypatch.setenv("RTK_PAIR", "1")
+    monkeypatch.setenv("RTK_POWER_F16", "1")
+    rng = np.random.default_rng(n * 11 + m)
+    M = rng.standard_normal((n, m))
+    if spread:
+        M *= 2.0 ** (-spread * rng.random(m))[None, :]
+    M = (M * scale).astype(np.float32)
+    Q = np.linalg.qr(rng.standard_normal((n, l)))[0].astype(np.float32)
+    Md = torch.from_numpy(np.asfortranarray(M)).cuda()
+    Y = power_step(Md, torch.from_numpy(Q).cuda()).cpu().numpy()
+    ref = M.astype(np.float64) @ (M.astype(np.float64).T @ Q.astype(np.float64))
+    assert np.all(np.isfinite(Y))
+    err = np.linalg.norm(Y - ref) / np.linalg.norm(ref)
+    assert err < TOL["fused"], err
+    colmax = np.maximum(np.max(np.abs(ref), axis=0), 1e-300)
+    ew = float(np.max(np.abs(Y - ref) / colmax[None, :]))
+    assert ew < TOL_EW["fused"], ew
+
+
 def test_power_step_padded_leading_dimension():
     torch = cuda_or_skip()
     from paper_2506_04840_b200 import power_step
