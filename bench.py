@@ -277,9 +277,11 @@ def run_ours(args, ws, rank, local):
     ms_prof = p0.elapsed_time(p1) / args.steps
     launches_per_step = int(prof.launches) / max(args.steps, 1)
 
-    # ---- roofline of the dominant kernel: the fused 3xTF32 power step on mode 1 ----
+    # ---- roofline of the dominant kernel: the fused power step on mode 1 ----
     # algorithmic work per launch (one power step): the unfolding read once,
-    # 4 n m bytes, and Y = M (M^T Q): 4 n m l flops, executed as 3 tf32 tensor products each
+    # 4 n m bytes, and Y = M (M^T Q): 4 n m l flops, executed as 3 tensor products each: fp16
+    # two-plane operands on the pair engine (kind::f16 runs at the bf16 rate), or
+    # 3xTF32 when RTK_PAIR_F16=0
     n, m, l = dims[0], 1, ranks[0] + p
     for j in dims[1:]:
         m *= j
@@ -291,11 +293,13 @@ def run_ours(args, ws, rank, local):
     hbm_peak = peaks["hbm_gbs"]
     bf16_burst = peaks.get("bf16_tflops", 1590.0)
     bf16_sus = peaks.get("bf16_tflops_sustained", bf16_burst)
-    # dense tf32 = bf16 / 2 (B200_PROFILING.md nominal ratio).  The kernel is timed alone-ish at
-    # full clocks inside a sub-second region, so the BURST figure is the denominator; the
-    # sustained one is reported beside it
-    tf32_peak = bf16_burst / 2.0
-    tf32_sus = bf16_sus / 2.0
+    # dense fp16 = bf16, dense tf32 = bf16 / 2 (B200_PROFILING.md nominal ratios).  The kernel is
+    # timed alone-ish at full clocks inside a sub-second region, so the BURST figure is the
+    # denominator; the sustained one is reported beside it
+    f16 = os.environ.get("RTK_PAIR_F16", "1") != "0"
+    tf32_peak = bf16_burst / (1.0 if f16 else 2.0)
+    tf32_sus = bf16_sus / (1.0 if f16 else 2.0)
+    prec = "3xFP16" if f16 else "3xTF32"
     t_hbm = bytes_alg / (hbm_peak * 1e9)
     t_tc = 3.0 * flops / (tf32_peak * 1e12)
     bound = "tensor" if t_tc >= t_hbm else "hbm"
@@ -317,12 +321,14 @@ def run_ours(args, ws, rank, local):
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": (achieved / peak) if achieved else None,
             "traffic": traffic,
-            "kernel": f"fused_power_kernel mode 1 (n={n}, m={m}, l={l}): single HBM pass, 3xTF32 tcgen05",
-            "algorithmic": {"bytes": bytes_alg, "flops_fp32": flops, "tf32_flops_3x": 3.0 * flops},
-            "peak_src": (f"tf32 dense = bf16 burst {bf16_burst:g}/2 TFLOP/s (MEASURED_PEAKS.json, {src}); "
-                         f"HBM {hbm_peak:g} GB/s"),
-            "frac_vs_sustained": (3.0 * flops / t_pow / 1e12) / tf32_sus if t_pow > 0 else None,
-            "sustained_peak": tf32_sus,
+            "kernel": (f"pair_power_kernel mode 1 (n={n}, m={m}, l={l}): single HBM pass on a CTA pair, "
+                       f"{prec} tcgen05"),
+            "algorithmic": {"bytes": bytes_alg, "flops_fp32": flops, "tensor_flops_3x": 3.0 * flops},
+            "peak_src": ((f"fp16 dense = bf16 burst {bf16_burst:g}" if f16 else f"tf32 dense = bf16 burst {bf16_burst:g}/2")
+                         + f" TFLOP/s (MEASURED_PEAKS.json, {src}); HBM {hbm_peak:g} GB/s (MEASURED_PEAKS.json)"),
+            "tensor_frac": (3.0 * flops / t_pow / 1e12) / tf32_peak if t_pow > 0 else None,
+            "tensor_frac_vs_sustained": (3.0 * flops / t_pow / 1e12) / tf32_sus if t_pow > 0 else None,
+            "sustained_tensor_peak": tf32_sus,
             "roofline_ms": max(t_hbm, t_tc) * 1e3,
             "launch_ms": t_pow * 1e3, "launches_timed": cnt,
             "timed_in": "separate profiled pass (CUDA events around each launch on its stream)",
@@ -404,7 +410,7 @@ def run_ours(args, ws, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "ms", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 stream / f64 small solves",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 stream (3xFP16 / 3xTF32 split products) / f64 small solves",
                 "data": "synthetic", "config": cfg_block(args.config, c),
                 "parallelism": f"replicas x{ws} (independent solves, no collective)",
                 "roofline": roof, "breakdown_ms_per_step": breakdown, "cpu_baseline": cpu,
@@ -473,7 +479,7 @@ def run_shard(args, ws, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": ms_step, "unit": "ms", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32 stream / f64 small solves",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32 stream (3xFP16 / 3xTF32 split products) / f64 small solves",
                 "data": "synthetic", "config": cfg_block(args.config, c),
                 "parallelism": f"last-mode shard x{ws}: n_{len(dims)} = {dims[-1]} split into slabs of "
                                f"{dims[-1] // ws}-{-(-dims[-1] // ws)} per GPU, one n_k x l fp64 all-reduce per "

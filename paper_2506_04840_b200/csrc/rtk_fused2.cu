@@ -66,7 +66,7 @@ __device__ unsigned long long g_pair_prof[2][32];
   do {                                                                                                  \
     const int _w = threadIdx.x >> 5;                                                                    \
     if (blockIdx.x < 2 && (threadIdx.x & 31) == 0 && ((slot) < 8 || (slot) >= 16 || _w == 2) &&         \
-        ((slot) < 20 || (slot) > 23 || _w == 10))                                                       \
+        ((slot) < 20 || (slot) > 27 || _w == 10))                                                       \
       atomicAdd(&g_pair_prof[blockIdx.x][slot], (unsigned long long)(clock64() - (t0)));                \
   } while (0)
 #else
@@ -165,7 +165,7 @@ __device__ __forceinline__ void p_wait_sleep(uint64_t* b, uint32_t phase) {
   uint32_t ok = 0;
   while (true) {
     asm volatile(
-        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
         "selp.u32 %0, 1, 0, P1;\n}\n"
         : "=r"(ok)
         : "r"(smem_addr(b)), "r"(phase)
@@ -308,6 +308,26 @@ __device__ __forceinline__ void p_tmem_st64u(uint32_t taddr, const uint32_t (&v)
       "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
       "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
       : "memory");
+}
+// 32 lanes x 32b, 64 consecutive columns, one wait
+__device__ __forceinline__ void p_tmem_ld64(uint32_t taddr, float (&v)[64]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),
+        "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),
+        "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 // warp max of v (>= 0), one atomicMax per warp on the float's bits (monotone for v >= 0)
 __device__ __forceinline__ void p_atomic_max(float* dst, float v) {
@@ -706,17 +726,23 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       const int b = NW == 2 ? (int)(jb & 1) : 0;
       { const long long _t0 = PCLK(); p_wait_sleep(&w_full[b], (uint32_t)((NW == 2 ? (jb >> 1) : jb) & 1)); PACC(21, _t0); }
       tc_fence_after();
+      const long long _tld0 = PCLK();
       float w[N];
+      if constexpr (N == 64) {
+        p_tmem_ld64(tbase + ((uint32_t)(32 * q) << 16) + 256 + b * N, w);
+      } else {
 #pragma unroll
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + 256 + b * N + c0, v);
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float v[16];
+          tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + 256 + b * N + c0, v);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) w[c0 + c] = v[c];
+          for (int c = 0; c < 16; ++c) w[c0 + c] = v[c];
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) p_arrive_cluster(wempty_c[b]);
+      PACC(25, _tld0);
       if (SHR) {
         // G x_k U_k^T: W(j, c) = sum_i M(i, j) U(i, c) is entry (c, j) of the shrunk unfolding; write
         // it at its place in the (k+1)-unfolding (Rprev x nnext x rest), rows padded to ldnext
@@ -771,7 +797,9 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       // column at 128 peer + j; hi = rna tf32, lo exact; once op2(jb-1) has released the planes
       { const long long _t0 = PCLK(); p_wait_sleep(&p_empty, (uint32_t)((jb & 1) ^ 1)); PACC(23, _t0); }
       const int ko = 128 * (int)rank + j, kp = 128 * (int)peer + j;
-      if constexpr (H) {   // fp16 planes [K/64][N2 c][64 k] (128-B rows, SW128), W scaled by tW
+      const long long _tpl0 = PCLK();
+      if (dbg & 32) {
+      } else if constexpr (H) {   // fp16 planes [K/64][N2 c][64 k] (128-B rows, SW128), W scaled by tW
         const uint32_t ro = (uint32_t)((ko >> 6) * (N2 * 128) + (((ko & 63) >> 3) << 4) + ((ko & 7) << 1));
         const uint32_t rp = (uint32_t)((kp >> 6) * (N2 * 128) + (((kp & 63) >> 3) << 4) + ((kp & 7) << 1));
 #pragma unroll
@@ -800,6 +828,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       }
       fence_async_smem();
       __syncwarp();
+      PACC(26, _tpl0);
       if (lane == 0) p_arrive_cluster(pfull_c);
     }
     PACC(20, _te0);
@@ -968,7 +997,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   PairArgs a;
   a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + KS - 1) / KS; a.nblk = nblk;
   a.Ypart = Ypart; a.stop = stop;
-  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : (H ? 4 : 8);   // stages (H: 64 rows each)
+  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : (H ? 2 : 8);   // stages (H: 64 rows each; 0-4 within 3 %, ncu)
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
   a.shrink = shrink_out ? 1 : 0;
   a.out = shrink_out;
@@ -1027,9 +1056,9 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
         fprintf(stderr,
                 "[pair prof cta%d] mma total %llu wait a_full(op1) %llu q_full %llu a_full(op2) %llu p_full %llu "
                 "w_empty %llu | prod total %llu r_full %llu a_empty %llu st %llu lds+split %llu arrive %llu walk %llu | tma r_empty %llu | epi total %llu "
-                "w_full %llu exch %llu p_empty %llu | q q_empty %llu\n",
+                "w_full %llu exch %llu p_empty %llu tmem_ld %llu planes %llu | q q_empty %llu\n",
                 r, h[r][0], h[r][1], h[r][2], h[r][3], h[r][4], h[r][5], h[r][8], h[r][9], h[r][10], h[r][11], h[r][12], h[r][13], h[r][14], h[r][17],
-                h[r][20], h[r][21], h[r][22], h[r][23], h[r][24]);
+                h[r][20], h[r][21], h[r][22], h[r][23], h[r][25], h[r][26], h[r][24]);
     unsigned long long z[2][32] = {};
     cudaMemcpyToSymbol(g_pair_prof, z, sizeof(z));
   }
@@ -1041,7 +1070,8 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
       case 16: return pair_launch<16, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
       case 32: return pair_launch<32, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
       case 48: return pair_launch<48, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
-      default: return pair_launch<64, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
+      default: return sa3 ? pair_launch<64, 3, true>(tq, ta, ta2, a, 2 * pairs, st)
+                          : pair_launch<64, 2, true>(tq, ta, ta2, a, 2 * pairs, st);
     }
   }
   switch (N) {
