@@ -97,6 +97,7 @@ struct PairArgs {
   const float* xmax_in;
   int cW;
   float* xmax_out; // tf32 sketch / shrink: atomicMax of max|M| (sketch) or of the written entries (shrink)
+  int op1pol;      // L2 policy of the power step's op1 tile loads: 0 evict_last, 1 evict_normal, 2 evict_first
 };
 
 // Stage order shared by the TMA, MMA and producer warps ("lagged" order):
@@ -438,7 +439,10 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
     // ---------------------------------------------------------------- TMA: A tiles (own ring)
     // walks the same segment sequence as the MMA warp: op1(0), [op1(1)], op2(0), op1(2), op2(1), ...
     if (lane == 0) {
-      const uint64_t pol_keep = p_policy_last(), pol_drop = p_policy_first();
+      const uint64_t pol_drop = p_policy_first();
+      uint64_t pol_keep = p_policy_last();
+      if (a.op1pol == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+      if (a.op1pol == 2) pol_keep = pol_drop;
       int sl = 0;
       uint32_t ph = 0;
       auto load = [&](int op, int x, int64_t y) {
@@ -1004,6 +1008,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   a.Rprev = Rprev; a.nnext = nnext; a.ldnext = ldnext;
   a.lk = l;
   a.sketch = sketch ? 1 : 0;
+  a.op1pol = getenv("RTK_PAIR_OP1POL") ? atoi(getenv("RTK_PAIR_OP1POL")) : 0;
   a.xmax_in = H ? ps->xmax_in : nullptr;
   a.xmax_out = (ps && (sketch || shrink_out)) ? ps->xmax_out : nullptr;
   if (a.xmax_out) ps->wrote = true;

@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 
 #include "rtk_gauss.cuh"
 #include "rtk_internal.h"
@@ -181,6 +182,13 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   y = y * fma(-0.5 * x * y, y, 1.5);
   y = y * fma(-0.5 * x * y, y, 1.5);
   return y;
+}
+// one Newton step (~2^-45 relative): the Cholesky pivots' 1/sqrt sits on the factorisation's serial
+// pivot chain; R and R^{-1} at ~1e-13 relative leave Q^T Q - I at that level, far below the fp32 stream
+__device__ __forceinline__ double rsqrt_1nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y * fma(-0.5 * x * y, y, 1.5);
 }
 __device__ __forceinline__ double rcp_fast(double x) {
   double y;
@@ -381,6 +389,159 @@ __device__ __noinline__ void tri_inv_upper(const double* R, double* T, int l, do
   __syncthreads();
   for (int idx = tid; idx < H * H; idx += kST) T[(H + idx / H) * kMLD + idx % H] = 0.0;
   __syncthreads();
+}
+
+// Blocked Cholesky G = R^T R together with T = R^{-1} (l <= 64), 8 x 8 blocks, nb = ceil(l / 8)
+// block steps.  R (ld kLD) and T (ld kMLD) come out as chol_upper / tri_inv_upper leave them: upper
+// triangular, zero below the diagonal, the identity beyond l.  Block step K: thread 0 factors the
+// updated diagonal block in registers -- R_KK and its inverse T_KK (1 / R_KK(k, k) is the pivot's
+// rsqrt) -- then one thread per panel column forms R_KJ = T_KK^T A_KJ, and all threads apply the
+// trailing update A_IJ -= R_KI^T R_KJ: three barriers per 8 columns against two per 4 columns plus
+// a separate substitution inverse, and a small rolled code body (the 18k-instruction step kernel
+// is fetched cold after every streaming pass, which evicts it from L2).  The off-diagonal blocks of
+// T follow along block anti-diagonals d = J - I: T_IJ = -T_II sum_{K = I+1..J} R_IK T_KJ.  Returns
+// false (uniformly) on a pivot <= 1e-13 max(diag G) or a non-finite pivot, the chol_upper rule.
+// flag: 32 doubles of scratch.
+__device__ unsigned long long g_chol_prof[8];   // phase cycles of chol_inv (RTK_CHOL=2, diagnostics)
+__device__ __noinline__ bool chol_inv(const double* A, double* R, double* T, double* flag, int l, int prof) {
+  const int tid = threadIdx.x;
+  long long c0 = clock64(), c1;
+#define CPROF(slot)                                                                     \
+  if (prof && tid == 0 && blockIdx.x == 0) {                                           \
+    c1 = clock64();                                                                     \
+    atomicAdd(&g_chol_prof[slot], (unsigned long long)(c1 - c0));                       \
+    c0 = c1;                                                                            \
+  }
+  const int nb = (l + 7) >> 3, L8 = 8 * nb;
+  double dmax = 0.0;
+  for (int k = 0; k < l; ++k) dmax = fmax(dmax, A[k * kLD + k]);
+  const double tol = 1e-13 * dmax;
+  for (int idx = tid; idx < kSL * kSL; idx += kST) {
+    const int i = idx / kSL, j = idx % kSL;
+    R[i * kLD + j] = (i < l && j < l) ? (j >= i ? A[i * kLD + j] : 0.0) : (i == j ? 1.0 : 0.0);
+    T[i * kMLD + j] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid == 0) flag[0] = 0.0;
+  __syncthreads();
+  CPROF(0);
+  for (int K = 0; K < nb; ++K) {
+    const int b = 8 * K;
+    if (tid == 0) {   // diagonal block: R_KK and T_KK in registers
+      double a[8][8], t[8][8], rs[8];
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[i][j] = j >= i ? R[(b + i) * kLD + b + j] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double piv = a[k][k];
+        if (!(piv > tol) || !(piv < DBL_MAX)) bad = true;
+        rs[k] = bad ? 0.0 : rsqrt_1nr(piv);
+        a[k][k] = piv * rs[k];
+#pragma unroll
+        for (int j = k + 1; j < 8; ++j) a[k][j] *= rs[k];
+#pragma unroll
+        for (int i = k + 1; i < 8; ++i)
+#pragma unroll
+          for (int j = i; j < 8; ++j) a[i][j] = fma(-a[k][i], a[k][j], a[i][j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        t[j][j] = rs[j];
+#pragma unroll
+        for (int i = j - 1; i >= 0; --i) {
+          double sm = 0.0;
+#pragma unroll
+          for (int m = i + 1; m <= j; ++m) sm = fma(a[i][m], t[m][j], sm);
+          t[i][j] = -sm * rs[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = i; j < 8; ++j) {
+          R[(b + i) * kLD + b + j] = a[i][j];
+          T[(b + i) * kMLD + b + j] = t[i][j];
+        }
+      if (bad) flag[0] = 1.0;
+    }
+    __syncthreads();
+    CPROF(1);
+    if (flag[0] != 0.0) return false;
+    const int S = L8 - b - 8;   // trailing columns
+    if (tid < S) {   // panel column c: R_KJ(:, c) = T_KK^T A_KJ(:, c)
+      const int c = b + 8 + tid;
+      double x[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) x[m] = R[(b + m) * kLD + c];
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        double y = 0.0;
+#pragma unroll
+        for (int m = 0; m <= i; ++m) y = fma(T[(b + m) * kMLD + b + i], x[m], y);
+        R[(b + i) * kLD + c] = y;
+      }
+    }
+    __syncthreads();
+    CPROF(2);
+    {   // trailing update of the upper triangle, one 4 x 4 block per thread (16 independent chains)
+      const int S4 = S >> 2;
+      const int bi = tid / 14, bj = tid % 14;   // S4 <= 14
+      if (bi < S4 && bj < S4 && bj >= bi) {
+        const int r0 = b + 8 + 4 * bi, c0 = b + 8 + 4 * bj;
+        double v[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[i][j] = R[(r0 + i) * kLD + c0 + j];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          double x[4], y[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { x[i] = R[(b + m) * kLD + r0 + i]; y[i] = R[(b + m) * kLD + c0 + i]; }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[i][j] = fma(-x[i], y[j], v[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (bj > bi || j >= i) R[(r0 + i) * kLD + c0 + j] = v[i][j];
+      }
+    }
+    __syncthreads();
+    CPROF(3);
+  }
+  for (int d = 1; d < nb; ++d) {   // T_IJ, J = I + d: one thread per block column
+    const int p = tid >> 3, j = tid & 7;
+    if (p < nb - d) {
+      const int I = p, J = p + d;
+      double P[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) P[i] = 0.0;
+      for (int K = I + 1; K <= J; ++K)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const double t = T[(8 * K + m) * kMLD + 8 * J + j];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) P[i] = fma(R[(8 * I + i) * kLD + 8 * K + m], t, P[i]);
+        }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double y = 0.0;
+#pragma unroll
+        for (int m = i; m < 8; ++m) y = fma(T[(8 * I + i) * kMLD + 8 * I + m], P[m], y);
+        T[(8 * I + i) * kMLD + 8 * J + j] = -y;
+      }
+    }
+    __syncthreads();
+  }
+  CPROF(4);
+#undef CPROF
+  return true;
 }
 
 // Householder tridiagonalisation H^T A H = tridiag(d, e) of the symmetric l x l A (read only).
@@ -880,6 +1041,8 @@ struct StepArgs {
   float* planes;            // [2 pN][pld] 3xTF32 planes of Q for the next op1 (nullptr: none)
   int pN, pld;
   int planes16;             // planes are the fp16 engine's: __half [2 pN][pld], Q scaled by 2^15
+  int chol_old;             // RTK_CHOL=0: the 4 x 4 Cholesky + substitution inverse (A/B only)
+  int chol_prof;            // RTK_CHOL=2: phase clocks of chol_inv into g_chol_prof
   double* alpha;
   double* trace;            // [q]
   double* sigma;            // [128]
@@ -1099,12 +1262,12 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   bool eig = a.final_step != 0 || stop;
   bool two_pass = false;
   if (!eig) {
-    const bool ok = chol_upper(S.G, S.R, S.rowbuf, l);
+    const bool ok = a.chol_old ? chol_upper(S.G, S.R, S.rowbuf, l) : chol_inv(S.G, S.R, S.T, S.rowbuf, l, a.chol_prof);
     tck[ntck++] = clock64();
     if (!ok) {
       eig = true;
     } else {
-      tri_inv_upper(S.R, S.T, l, S.rowbuf);
+      if (a.chol_old) tri_inv_upper(S.R, S.T, l, S.rowbuf);
       tck[ntck++] = clock64();
       // kappa_F(R) = ||R||_F ||R^{-1}||_F >= kappa_2(Y); one CholQR pass leaves
       // ||Q^T Q - I|| ~ eps kappa^2
@@ -1310,7 +1473,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     }
     cluster.sync();
     load_packed_sum(a.g2part, C, np, l, S.G);
-    const bool ok2 = chol_upper(S.G, S.R, S.rowbuf, l);
+    const bool ok2 = a.chol_old ? chol_upper(S.G, S.R, S.rowbuf, l) : chol_inv(S.G, S.R, S.T, S.rowbuf, l, a.chol_prof);
     if (!ok2) {
       if (rank == 0 && tid == 0) a.status[0] = 6;   // RTK_ERR_NUMERIC
       for (int idx = tid; idx < kSL * kSL; idx += kST) {
@@ -1318,7 +1481,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
         S.T[k * kMLD + c] = (k == c) ? 1.0 : 0.0;
       }
       __syncthreads();
-    } else {
+    } else if (a.chol_old) {
       tri_inv_upper(S.R, S.T, l, S.rowbuf);
     }
     for (int i0 = r0; i0 < r1; i0 += kChunk) {
@@ -1817,6 +1980,23 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   a.nblk = gram_blocks(B.n);
   a.gpart = B.gpart; a.Y = B.Y; a.Q1 = B.Q1; a.g2part = B.g2part; a.gsum = B.gsum; a.amax = B.amax;
   a.Qd = B.Qd; a.Qs = B.Qs; a.planes = planes; a.pN = pN; a.pld = pld; a.planes16 = planes16 ? 1 : 0;
+  {
+    const char* ce = getenv("RTK_CHOL");
+    // the blocked 8 x 8 version wins for l <= 40 (C3 1.70 -> 1.68 ms, C4 1.91 -> 1.83), the 4 x 4 one
+    // with the substitution inverse at l = 60 (C5 9.62 vs 9.69): its 15 short pivot blocks pipeline
+    // better than 8 single-thread 8 x 8 factorisations on the fp64 latency chain
+    a.chol_old = (ce && ce[0] == '0') || (!(ce && ce[0] >= '1') && B.l > 40) ? 1 : 0;
+    a.chol_prof = (ce && ce[0] == '2') ? 1 : 0;
+    static int calls = 0;
+    if (a.chol_prof && calls++ > 0) {   // report the previous launch and reset
+      unsigned long long h[8];
+      cudaMemcpyFromSymbol(h, g_chol_prof, sizeof(h));
+      fprintf(stderr, "[chol_inv prof, previous launch, CTA 0] init %llu diag %llu panel %llu trail %llu inverse %llu\n",
+              h[0], h[1], h[2], h[3], h[4]);
+      unsigned long long z[8] = {};
+      cudaMemcpyToSymbol(g_chol_prof, z, sizeof(z));
+    }
+  }
   a.alpha = B.alpha; a.trace = B.trace; a.sigma = B.sigma; a.status = B.status;
   a.U = U; a.seed = seed; a.mode1 = mode1;
   a.dbg = g_step_dbg;
