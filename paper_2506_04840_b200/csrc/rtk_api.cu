@@ -523,8 +523,9 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
         B.G = Gf; B.ltot = tc_npad(l); B.n_rows = rows;
       } else {
       const int G2 = tc_op2_grid(v, G);
-      if (step == 0) {
-        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G2, st, om));
+      if (step == 0) {   // (records max|M| for the fp16 pair power steps, like the pair sketch)
+        RTK_CK(tc_op2(v, l, nullptr, 0, true, seed, mode1, B.Ypart, G2, st, om, h16c ? xs->xmax + k : nullptr));
+        if (h16c) xs->ready[k] = 1;
         g_launches += 1;
       } else {
         if (!fast) RTK_CK(tc_split(B.Qd, nullptr, n, l, planes, st));   // else: written by step_kernel

@@ -84,7 +84,8 @@ struct PairArgs {
   const int* stop; // Alg. B.1 stop flag (nullptr: none)
   int lag;         // op1(b+1) stages issued before op2(b) (the lagged order, PSeg)
   int dbg;         // ablations (RTK_PAIR_DBG, timing only, results wrong): 1 no MMAs, 2 no A loads,
-                   // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads
+                   // 4 producers skip LDS, 8 producers skip TMEM stores, 16 no Q loads, 32 no W-plane
+                   // writes, 64 no op1 A loads, 128 no op2 A loads
   int shrink;      // 1: the mode-k shrink G x_k U_k^T -- op1 only (W = M_J^T U), each CTA writes its
                    // 128 columns' W rows as the next unfolding (no exchange, no op2, no Y)
   float* out;      // shrink output (column-major, leading dimension ldnext)
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       auto load = [&](int op, int x, int64_t y) {
         { const long long _t0 = PCLK(); bar_wait(&r_empty[sl], ph ^ 1); PACC(17, _t0); }
         uint8_t* dst = smR + sl * SLOT;
-        if (dbg & 2) {
+        if ((dbg & 2) || (op == 1 && (dbg & 64)) || (op == 2 && (dbg & 128))) {
           bar_arrive(&r_full[sl]);
         } else {
           bar_expect_tx(&r_full[sl], SLOT);
@@ -465,7 +466,9 @@ __global__ void __launch_bounds__(kPThreads, 1) pair_power_kernel(const __grid_c
       const int L = lagL;
       auto seg1 = [&](int64_t blk, int k0, int k1) {   // all rows of this CTA's 128 columns
         const int64_t y = colbase(blk) + 128 * rank;
-        for (int k = k0; k < k1; ++k) load(1, KS * k, y);
+        for (int k = k0; k < k1; ++k) {
+          load(1, KS * k, y);
+        }
       };
       auto seg2 = [&](int64_t blk) {                    // this CTA's rows of each pair-tile x 256 columns
         const int64_t c0 = colbase(blk);

@@ -121,7 +121,7 @@ cudaError_t tc_split(const double* q64, const float* q32, int n, int l, float* p
 cudaError_t tc_op1(const View& v, int l, const float* planes, float* W, int64_t ldw, bool shrink, float* out,
                    int64_t Rprev, int64_t nnext, int64_t ldnext, cudaStream_t st, int max_ctas = 0);
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
-                   float* Ypart, int G, cudaStream_t st, const float* om = nullptr);
+                   float* Ypart, int G, cudaStream_t st, const float* om = nullptr, float* xmax = nullptr);
 
 // The fp16 two-plane power step and its scale (rtk_fused2.cu): xmax_in = max|M| of the
 // unfolding (device) selects it for a power step (planes are then fp16 [2N][pld], pld % 8 == 0, scaled

@@ -58,6 +58,7 @@ struct TcOp2Args {
   int sketch;
   uint64_t seed;
   uint32_t mode;
+  float* xmax;         // sketch: atomicMax of max|M| (the fp16 pair engine's scale, rtk_fused2.cu)
   const float* om;   // materialised Omega_k [m][l] or nullptr (RTK-GAUSS-1 in place)
 };
 
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
   } else if (warp < 6) {
     const int tid = threadIdx.x - 64;    // 0..127
     int64_t ia = 0;
+    float vmax = 0.f;
     for (int64_t kc = k0; kc < k1; ++kc) {
       const int64_t ib = kc - k0;
       if (a.sketch) {
@@ -361,11 +363,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_op2_kernel(const __grid_cons
           const float4 v = src[tid + 128 * r];
           dst[tid + 128 * r] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
                                            v.w - tf32_trunc(v.w));
+          if (a.xmax) vmax = fmaxf(fmaxf(vmax, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) bar_arrive(&loA[s]);
       }
+    }
+    if (a.xmax) {   // every element of M passes through one split warp of one CTA
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+      if (lane == 0) atomicMax(reinterpret_cast<unsigned int*>(a.xmax), __float_as_uint(vmax));
     }
   } else {
     // ---------------- epilogue: partial Y of this CTA -> Ypart[grp][c][i]
@@ -536,7 +544,7 @@ int tc_op2_grid(const View& v, int G) {
 
 // op2: Ypart[G][N][nit*128] = per-CTA partial M W (or M Omega_k when sketch)
 cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketch, uint64_t seed, uint32_t mode,
-                   float* Ypart, int G, cudaStream_t st, const float* om) {
+                   float* Ypart, int G, cudaStream_t st, const float* om, float* xmax) {
   const int N = tc_npad(l);
   CUtensorMap mM, mB;
   if (!make_map(&mM, v.base, (uint64_t)v.n, (uint64_t)v.m(), (uint64_t)v.ss, 32, 32,
@@ -550,6 +558,7 @@ cudaError_t tc_op2(const View& v, int l, const float* W, int64_t ldw, bool sketc
   TcOp2Args a;
   a.n = v.n; a.N = N; a.l = l; a.m = v.m(); a.nit = (v.n + 127) / 128; a.nkc = (v.m() + kBK - 1) / kBK;
   a.G = G; a.Ypart = Ypart; a.sketch = sketch ? 1 : 0; a.seed = seed; a.mode = mode; a.om = om;
+  a.xmax = sketch ? xmax : nullptr;
   switch (N) {
     case 16: return op2_launch<16>(mM, mB, a, G, st);
     case 32: return op2_launch<32>(mM, mB, a, G, st);
