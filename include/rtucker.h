@@ -7,7 +7,7 @@
  *   Alg. 4 "shifted randomized ST-HOSVD"  PAPER.md:293-313   -> rtk_rsthosvd
  *   Alg. 2 (alpha = 0) and Alg. B.1 (PVE stop,
  *   PAPER.md:1145-1172) through rtk_solve() options.
- * Per mode k (order 1..d): Omega_k (RTK-GAUSS-1),
+ * Per mode k (order 1..d): Omega_k (RTK-GAUSS-2),
  * Y = M Omega_k, Q = orth(Y), alpha = 0; q times { Y = M (M^T Q) - alpha Q;
  * [Q,Sigma] = svd(Y); if Sigma(l,l) > alpha: alpha = (Sigma(l,l)+alpha)/2 };
  * U_k = Q(:,1:r_k) (sign-pinned); M = A_(k) (Alg. 3) or G_(k) (Alg. 4), and
@@ -111,7 +111,7 @@ typedef struct rtk_options {
                        * l_k <= 64 and l_k <= min(n_k, m_k) with m_k over l_1..l_{k-1}
                        * (RTK_ERR_ARG / RTK_ERR_SHAPE otherwise). */
   int32_t omega;      /* sketch type (Appendix D): 0 standard Gaussian
-                       * (RTK-GAUSS-1, generated inside the sketch kernels), 1 uniform U[-1,1]
+                       * (RTK-GAUSS-2, generated inside the sketch kernels), 1 uniform U[-1,1]
                        * (RTK-UNIF-1), 2 Khatri-Rao product of Gaussian factors, 3 Khatri-Rao
                        * product of uniform factors (RTK-KR-1); types 1-3 are materialised once per
                        * mode in the workspace (rtk_workspace_bytes_ex sizes it) */
@@ -125,7 +125,7 @@ typedef struct rtk_options {
  *   ranks  host, d entries r_k in [1, n_k]
  *   p      oversampling s_k (same for all modes), l_k = r_k + p
  *   q      power steps >= 1
- *   seed   Omega seed (RTK-GAUSS-1 key); mode k uses counter word 3 = k (1-based)
+ *   seed   Omega seed (RTK-GAUSS-2 key); mode k uses counter word 3 = k (1-based)
  *   U      host array of d DEVICE pointers, U[k] -> n_k x r_k float32 (written)
  *   core   device, r_1 x ... x r_d float32 (written); core = A x_1 U_1^T ... x_d U_d^T
  *   ws     device workspace of ws_bytes (>= rtk_workspace_bytes), or NULL
@@ -184,7 +184,7 @@ RTK_API size_t rtk_workspace_bytes_shard(const rtk_options* opt, const int64_t* 
 RTK_API size_t rtk_workspace_bytes_ex(const rtk_options* opt, const int64_t* dims, int32_t d,
                                       const int32_t* ranks, int32_t p, int32_t q);
 
-/* Test hook: rows [row0, row0+rows) of Omega_mode (l columns) in RTK-GAUSS-1,
+/* Test hook: rows [row0, row0+rows) of Omega_mode (l columns) in RTK-GAUSS-2,
  * written row-major to the DEVICE buffer out[(j-row0)*l + c] (float32). */
 RTK_API int rtk_omega(uint64_t seed, int32_t mode, int64_t row0, int64_t rows, int32_t l, float* out,
               void* stream);

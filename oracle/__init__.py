@@ -6,13 +6,13 @@ from this package.  The product path (``paper_2506_04840_b200``) never imports
 it and fails loudly when its CUDA library is missing.
 
 The oracle shares no code with the CUDA path.  Both sides implement the same
-written specification of the sketch generator (DESIGN.md "RTK-GAUSS-1"); the
+written specification of the sketch generator (DESIGN.md "RTK-GAUSS-2"); the
 seeded input generators live in ``workloads/`` and contain none of the
 method's arithmetic.
 
 Modules
 -------
-gauss   Philox4x32-10 + RTK-GAUSS-1 Box-Muller (the Omega_k of Alg. 3/4,
+gauss   Philox4x32-10 + RTK-GAUSS-2 Box-Muller (the Omega_k of Alg. 3/4,
         PAPER.md:257, :300).
 tucker  unfold / fold / mode-k product, Alg. 1
         (PAPER.md:113-125), Alg. 2 (PAPER.md:211-237), Alg. 3

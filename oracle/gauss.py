@@ -1,11 +1,11 @@
-"""Oracle sketch generator: Philox4x32-10 + the frozen RTK-GAUSS-1 Box-Muller.
+"""Oracle sketch generator: Philox4x32-10 + the frozen RTK-GAUSS-2 Box-Muller.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 The paper draws "a standard Gaussian matrix Omega_k" afresh for every mode
 (Alg. 3 line 3; Alg. 4 line 3; definition of a
 standard Gaussian matrix PAPER.md:96).  It names no generator, so this build
-freezes one (SURVEY.md 8(c) reading C2, restated in DESIGN.md "RTK-GAUSS-1"):
+freezes one (SURVEY.md 8(c) reading C2, restated in DESIGN.md "RTK-GAUSS-2"):
 
   key     = (lo32(seed), hi32(seed))
   counter = (c // 4, lo32(j), hi32(j), k)     j = canonical unfolding column,
@@ -13,19 +13,23 @@ freezes one (SURVEY.md 8(c) reading C2, restated in DESIGN.md "RTK-GAUSS-1"):
   x0..x3  = Philox4x32-10(counter, key)       (Salmon et al. 2011)
   (x0,x1) -> Box-Muller pair -> columns 4*(c//4)+0, +1
   (x2,x3) -> Box-Muller pair -> columns 4*(c//4)+2, +3
-  u       = ((x >> 8) + 0.5) * 2^-24          (exact in float64, u in (0,1))
+  u       = (2 (x >> 9) + 1) * 2^-24          (exact in binary32, u in (0,1))
   z0      = sqrt(-2 ln u_a) cos(2 pi u_b),  z1 = sqrt(-2 ln u_a) sin(2 pi u_b)
 
 ln, sin and cos are evaluated with the fixed range reductions and fixed
-polynomials below using only IEEE-754 binary64 +, -, *, / and sqrt, each
-correctly rounded and never fused, in exactly the order written here.  The
-float64 Gaussian is rounded to float32 (round-to-nearest-even); Omega_k is that
-float32 value.  The CUDA side implements the same written spec independently
-(no shared code); the two must agree bit for bit.
+polynomials below using only IEEE-754 binary32 +, -, *, / and sqrt, each
+correctly rounded and never fused, in exactly the order written here; Omega_k
+is the binary32 z.  The constants are the correctly rounded binary32 values of
+the stated rationals, frozen as bit patterns.  The CUDA side implements the
+same written spec independently (no shared code); the two must agree bit for
+bit.  (RTK-GAUSS-1, the first frozen version, did the same in binary64 with
+25-bit uniforms; binary32 needs about a third of the issue slots and keeps the
+Gaussians accurate to a few binary32 ulp, far below what a sketch needs.)
 
 Pins (tests/test_oracle_gauss.py): Philox against an independently compiled
 cuRAND ``curand_Philox4x32_10`` and published known-answer vectors; ln/sin/cos
-against libm (numpy) to <= 4 ulp; moments and a KS test of the Gaussians.
+against libm (numpy float64) to <= 4 binary32 ulp / 3e-7; moments and a KS
+test of the Gaussians.
 """
 from __future__ import annotations
 
@@ -66,94 +70,93 @@ def philox4x32_10(c0, c1, c2, c3, k0, k1):
             c2.astype(np.uint32), c3.astype(np.uint32))
 
 
-# ---- RTK-GAUSS-1 constants (binary64, written as hex so both sides agree) ----
-LN2_HI = float.fromhex("0x1.62e42fee00000p-1")
-LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
-SQRT2 = float.fromhex("0x1.6a09e667f3bcdp+0")
-PIO2 = float.fromhex("0x1.921fb54442d18p+0")
-TWO_M23 = float.fromhex("0x1p-23")
-# ln: 2 s * sum_{k=0..11} z^k/(2k+1)
-LOG_C = [1.0 / (2 * k + 1) for k in range(12)]
-# sin: x * sum_{k=0..8} (-1)^k y^k/(2k+1)!    cos: sum_{k=0..9} (-1)^k y^k/(2k)!
-def _fact(n):
-    f = 1.0
-    for i in range(2, n + 1):
-        f = f * float(i)          # exact: every n! used here is < 2^53
-    return f
-SIN_C = [(-1.0 if k % 2 else 1.0) / _fact(2 * k + 1) for k in range(9)]
-COS_C = [(-1.0 if k % 2 else 1.0) / _fact(2 * k) for k in range(10)]
+# ---- RTK-GAUSS-2 constants (binary32 bit patterns, so both sides agree) ----
+def _f32(bits):
+    return np.array([bits], dtype=np.uint32).view(np.float32)[0]
+
+
+LN2_HI = _f32(0x3F317200)      # 0.693145751953125 (16 significant bits: n*LN2_HI exact for |n| <= 24)
+LN2_LO = _f32(0x35BFBE8E)      # ln 2 - LN2_HI rounded
+SQRT2 = _f32(0x3FB504F3)       # fl32(sqrt 2)
+PIO2 = _f32(0x3FC90FDB)        # fl32(pi / 2)
+# ln: 2 s * sum_{k=0..4} z^k/(2k+1);  sin: x * sum_{k=0..4} (-1)^k y^k/(2k+1)!;
+# cos: sum_{k=0..5} (-1)^k y^k/(2k)!   (correctly rounded binary32 of each rational)
+LOG_C = [_f32(b) for b in (0x3F800000, 0x3EAAAAAB, 0x3E4CCCCD, 0x3E124925, 0x3DE38E39)]
+SIN_C = [_f32(b) for b in (0x3F800000, 0xBE2AAAAB, 0x3C088889, 0xB9500D01, 0x3638EF1D)]
+COS_C = [_f32(b) for b in (0x3F800000, 0xBF000000, 0x3D2AAAAB, 0xBAB60B61, 0x37D00D01, 0xB493F27E)]
+_F = np.float32
 
 
 def _odd_int(x):
-    """x (uint32) -> v = 2*(x>>8)+1, an odd integer in [1, 2^25); u = v*2^-25."""
-    return (np.asarray(x, dtype=np.uint64) >> np.uint64(8)) * np.uint64(2) + np.uint64(1)
+    """x (uint32) -> v = 2*(x>>9)+1, an odd integer in [1, 2^24); u = v*2^-24."""
+    return (np.asarray(x, dtype=np.uint64) >> np.uint64(9)) * np.uint64(2) + np.uint64(1)
 
 
 def uniform01(x):
-    """u = ((x>>8)+0.5)*2^-24, exact in binary64."""
-    return _odd_int(x).astype(np.float64) * float.fromhex("0x1p-25")
+    """u = (2(x>>9)+1)*2^-24, exact in binary32."""
+    return _odd_int(x).astype(np.float32) * _F(2.0**-24)
 
 
 def rtk_log_u(x):
-    """ln(u) for u = ((x>>8)+0.5)*2^-24 using the RTK-GAUSS-1 recipe.
+    """ln(u) for u = (2(x>>9)+1)*2^-24 using the RTK-GAUSS-2 recipe (binary32).
 
-    v = 2(x>>8)+1 (odd, < 2^25); e = floor(log2 v); f = v*2^-e in [1,2) (exact);
-    if f > SQRT2: f = f/2, e = e+1 (exact);  s = (f-1)/(f+1); z = s*s;
-    p = Horner(LOG_C, z); lnf = (2*s)*p;  ln u = (e-25)*LN2_HI + ((e-25)*LN2_LO + lnf).
+    v = 2(x>>9)+1 (odd, < 2^24); e = floor(log2 v); f = v*2^-e in [1,2) (exact);
+    if f > SQRT2: f = f*0.5, e = e+1 (exact);  s = (f-1)/(f+1); z = s*s;
+    p = Horner(LOG_C, z); lnf = (2*s)*p;  ln u = (e-24)*LN2_HI + ((e-24)*LN2_LO + lnf).
     """
     v = _odd_int(x)
-    # e = bit_length(v) - 1 = #{b in 1..24 : v >> b != 0}   (integer arithmetic)
+    # e = bit_length(v) - 1 = #{b in 1..23 : v >> b != 0}   (integer arithmetic)
     e = np.zeros(v.shape, dtype=np.int64)
-    for b in range(1, 25):
+    for b in range(1, 24):
         e += ((v >> np.uint64(b)) != 0).astype(np.int64)
-    f = v.astype(np.float64) * np.ldexp(1.0, -e)
+    f = v.astype(np.float32) * np.ldexp(_F(1.0), -e).astype(np.float32)
     big = f > SQRT2
-    f = np.where(big, f * 0.5, f)
+    f = np.where(big, f * _F(0.5), f).astype(np.float32)
     e = np.where(big, e + 1, e)
-    s = (f - 1.0) / (f + 1.0)
+    s = (f - _F(1.0)) / (f + _F(1.0))
     z = s * s
-    p = np.full_like(z, LOG_C[11])
-    for k in range(10, -1, -1):
+    p = np.full_like(z, LOG_C[4])
+    for k in range(3, -1, -1):
         p = p * z + LOG_C[k]
-    lnf = (2.0 * s) * p
-    n = (e - 25).astype(np.float64)
+    lnf = (_F(2.0) * s) * p
+    n = (e - 24).astype(np.float32)
     return n * LN2_HI + (n * LN2_LO + lnf)
 
 
 def rtk_sincos_2pi_u(x):
-    """(sin(2 pi u), cos(2 pi u)) for u = ((x>>8)+0.5)*2^-24, RTK-GAUSS-1 recipe.
+    """(sin(2 pi u), cos(2 pi u)) for u = (2(x>>9)+1)*2^-24, RTK-GAUSS-2 recipe (binary32).
 
-    w = 2(x>>8)+1; quadrant qd = w>>23; rem = w & (2^23-1); t = rem*2^-23 (exact);
-    if rem < 2^22: x = t*PIO2, (S,C) = (sin x, cos x)
+    w = 2(x>>9)+1; quadrant qd = w>>22; rem = w & (2^22-1); t = rem*2^-22 (exact);
+    if rem < 2^21: x = t*PIO2, (S,C) = (sin x, cos x)
     else:          x = (1-t)*PIO2, (S,C) = (cos x, sin x)
     sin x = x*Horner(SIN_C, x*x); cos x = Horner(COS_C, x*x);
     quadrant: qd=0 -> (S,C); 1 -> (C,-S); 2 -> (-S,-C); 3 -> (-C,S)  as (sin,cos).
     """
     w = _odd_int(x)
-    qd = (w >> np.uint64(23)).astype(np.int64)
-    rem = w & np.uint64((1 << 23) - 1)
-    t = rem.astype(np.float64) * TWO_M23
-    low = rem < np.uint64(1 << 22)
-    xr = np.where(low, t, 1.0 - t) * PIO2
+    qd = (w >> np.uint64(22)).astype(np.int64)
+    rem = w & np.uint64((1 << 22) - 1)
+    t = rem.astype(np.float32) * _F(2.0**-22)
+    low = rem < np.uint64(1 << 21)
+    xr = np.where(low, t, _F(1.0) - t).astype(np.float32) * PIO2
     y = xr * xr
-    ps = np.full_like(y, SIN_C[8])
-    for k in range(7, -1, -1):
+    ps = np.full_like(y, SIN_C[4])
+    for k in range(3, -1, -1):
         ps = ps * y + SIN_C[k]
     sx = xr * ps
-    pc = np.full_like(y, COS_C[9])
-    for k in range(8, -1, -1):
+    pc = np.full_like(y, COS_C[5])
+    for k in range(4, -1, -1):
         pc = pc * y + COS_C[k]
     cx = pc
     S = np.where(low, sx, cx)
     C = np.where(low, cx, sx)
-    sin_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [S, C, -S, -C])
-    cos_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [C, -S, -C, S])
+    sin_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [S, C, -S, -C]).astype(np.float32)
+    cos_o = np.select([qd == 0, qd == 1, qd == 2, qd == 3], [C, -S, -C, S]).astype(np.float32)
     return sin_o, cos_o
 
 
 def box_muller(xa, xb):
-    """RTK-GAUSS-1 pair: r = sqrt(-2*ln u_a); (r*cos(2 pi u_b), r*sin(2 pi u_b)) in float64."""
-    r = np.sqrt(-2.0 * rtk_log_u(xa))
+    """RTK-GAUSS-2 pair: r = sqrt(-2*ln u_a); (r*cos(2 pi u_b), r*sin(2 pi u_b)) in binary32."""
+    r = np.sqrt(_F(-2.0) * rtk_log_u(xa))
     s, c = rtk_sincos_2pi_u(xb)
     return r * c, r * s
 
@@ -163,7 +166,7 @@ def omega(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
 
     Row index = canonical unfolding column j (Kolda-Bader order, SURVEY.md 8(c)
     C3); mode = 1-based mode index k in processing order.  Follows PAPER.md:257
-    ("Draw a standard Gaussian matrix Omega_k") with the RTK-GAUSS-1 stream.
+    ("Draw a standard Gaussian matrix Omega_k") with the RTK-GAUSS-2 stream.
     """
     j = np.arange(row0, row0 + rows, dtype=np.uint64)
     n4 = (l + 3) // 4
@@ -184,7 +187,7 @@ def omega(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
 
 # ------------------------------------------------------------------ other sketch types
 # PAPER.md:1377-1379 (Appendix D) compares Omega_k drawn as: a standard Gaussian matrix (the
-# main algorithms, RTK-GAUSS-1 above), a uniform random matrix (entries i.i.d. U[-1, 1]), and
+# main algorithms, RTK-GAUSS-2 above), a uniform random matrix (entries i.i.d. U[-1, 1]), and
 # the Khatri-Rao product of standard Gaussian / uniform matrices.  The paper fixes neither a
 # generator nor the Khatri-Rao ordering; this build freezes (readings C2, C19):
 #
@@ -195,7 +198,7 @@ def omega(seed: int, mode: int, row0: int, rows: int, l: int) -> np.ndarray:
 #             (Kolda-Bader: lower modes fastest, extents of the CURRENT tensor), i.e. the
 #             Khatri-Rao product F_d (.) ... (.) F_1 without F_k.  f_m is an n_m x l matrix
 #             drawn row by row like Omega itself with counter word 3 =
-#             0x4B000000 | (m << 8) | k  (Gaussian, RTK-GAUSS-1 pairs) or
+#             0x4B000000 | (m << 8) | k  (Gaussian, RTK-GAUSS-2 pairs) or
 #             0x4C000000 | (m << 8) | k  (uniform, RTK-UNIF-1 words).
 OMEGA_GAUSS, OMEGA_UNIF, OMEGA_KR_GAUSS, OMEGA_KR_UNIF = 0, 1, 2, 3
 

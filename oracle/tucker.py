@@ -115,7 +115,7 @@ def _range_finder(m: np.ndarray, r: int, p: int, q: int, seed: int, mode1: int,
     """Lines 3-13 of Alg. 3 / Alg. 4 for one mode.
 
     m      : the matrix being factored, A_(k) (Alg. 3) or G_(k) (Alg. 4), float64
-    mode1  : 1-based mode index (Philox counter word, DESIGN.md RTK-GAUSS-1)
+    mode1  : 1-based mode index (Philox counter word, DESIGN.md RTK-GAUSS-2)
     shift  : False -> Alg. 2 (alpha fixed at 0)
     pve_tol: (tol, q_max) -> Alg. B.1 stopping rule
     full   : return the whole n x l basis Q_k of the last iterate (Alg. A.2 line 12), unpinned

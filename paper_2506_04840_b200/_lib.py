@@ -304,7 +304,7 @@ def rsthosvd_a2(A, ranks, p: int, q: int, seed: int, **kw):
 
 
 def omega(seed: int, mode: int, row0: int, rows: int, l: int, device="cuda"):
-    """Rows [row0, row0+rows) of Omega_mode (RTK-GAUSS-1) computed by the CUDA kernel."""
+    """Rows [row0, row0+rows) of Omega_mode (RTK-GAUSS-2) computed by the CUDA kernel."""
     import torch
     lib = load_library()
     out = torch.empty((rows, l), dtype=torch.float32, device=device)

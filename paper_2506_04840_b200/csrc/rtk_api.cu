@@ -108,7 +108,7 @@ struct Problem {
   bool seq = true;
   double pve = 0.0;   // > 0: Alg. B.1 tolerance, q is q_max
   bool a2 = false;    // Alg. A.2: each mode keeps all l_k columns, then ST-HOSVD of the l-core
-  int omega = 0;      // sketch type: 0 RTK-GAUSS-1, 1 uniform, 2 KR-Gaussian, 3 KR-uniform
+  int omega = 0;      // sketch type: 0 RTK-GAUSS-2, 1 uniform, 2 KR-Gaussian, 3 KR-uniform
   std::vector<int> keep;   // columns kept by mode k's shrink: r_k, or l_k = r_k + p (A.2)
   // multi-GPU last-mode shard: dims[d-1] is this rank's slab, full_last the whole
   // extent, sh_begin the slab's first index; modes < d-1 all-reduce Y after every streaming pass

@@ -1,14 +1,14 @@
-// rtk_gauss.cuh -- device implementation of the RTK-GAUSS-1 sketch stream.
+// rtk_gauss.cuh -- device implementation of the RTK-GAUSS-2 sketch stream.
 //
 // Omega_k(j, c) for the standard Gaussian sketch of Alg. 3 / Alg. 4 line 3
 // ("standard Gaussian matrix" PAPER.md:96).  Written from
 // the DESIGN.md specification, independently of the oracle: Philox4x32-10
 // (Salmon et al. 2011) on counter (c/4, lo32(j), hi32(j), k) and key
 // (lo32(seed), hi32(seed)), then a Box-Muller pair per two outputs whose ln,
-// sin, cos use only correctly rounded, never fused binary64 + - * / sqrt
-// (__dadd_rn / __dmul_rn / __ddiv_rn / __dsqrt_rn) in the specified order, and
-// a final round-to-nearest to float32.  Bit-identical to the spec by
-// construction; tests/test_gpu_omega.py checks it against the oracle.
+// sin, cos use only correctly rounded, never fused binary32 + - * / sqrt
+// (__fadd_rn / __fmul_rn / __fdiv_rn / __fsqrt_rn) in the specified order.
+// Bit-identical to the spec by construction; tests/test_gpu_kernels.py checks
+// it against the oracle.
 #pragma once
 #include <cstdint>
 
@@ -28,76 +28,64 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-// ---- spec constants -------------------------------------------------------
-constexpr double kLn2Hi = 0x1.62e42fee00000p-1;
-constexpr double kLn2Lo = 0x1.a39ef35793c76p-33;
-constexpr double kSqrt2 = 0x1.6a09e667f3bcdp+0;
-constexpr double kPiO2 = 0x1.921fb54442d18p+0;
-
-// Spec coefficients, written as correctly rounded quotients of exact integers
-// (every factorial below is < 2^53):  ln: c_k = 1/(2k+1), k = 0..11;
-// sin: (-1)^k/(2k+1)!, k = 0..8;  cos: (-1)^k/(2k)!, k = 0..9.
-__host__ __device__ constexpr double log_c(int k) {
-  return k == 0 ? 1.0 : k == 1 ? 1.0 / 3.0 : k == 2 ? 1.0 / 5.0 : k == 3 ? 1.0 / 7.0
-       : k == 4 ? 1.0 / 9.0 : k == 5 ? 1.0 / 11.0 : k == 6 ? 1.0 / 13.0 : k == 7 ? 1.0 / 15.0
-       : k == 8 ? 1.0 / 17.0 : k == 9 ? 1.0 / 19.0 : k == 10 ? 1.0 / 21.0 : 1.0 / 23.0;
+// ---- spec constants (binary32 bit patterns, DESIGN.md RTK-GAUSS-2) ------------
+__device__ __forceinline__ float f32b(uint32_t b) { return __uint_as_float(b); }
+constexpr uint32_t kLn2Hi = 0x3F317200u;   // 0.693145751953125
+constexpr uint32_t kLn2Lo = 0x35BFBE8Eu;
+constexpr uint32_t kSqrt2 = 0x3FB504F3u;
+constexpr uint32_t kPiO2 = 0x3FC90FDBu;
+// correctly rounded binary32 of ln: 1/(2k+1), k = 0..4;  sin: (-1)^k/(2k+1)!, k = 0..4;
+// cos: (-1)^k/(2k)!, k = 0..5
+__device__ __forceinline__ float log_c(int k) {
+  return f32b(k == 0 ? 0x3F800000u : k == 1 ? 0x3EAAAAABu : k == 2 ? 0x3E4CCCCDu : k == 3 ? 0x3E124925u : 0x3DE38E39u);
 }
-__host__ __device__ constexpr double sin_c(int k) {
-  return k == 0 ? 1.0 : k == 1 ? -1.0 / 6.0 : k == 2 ? 1.0 / 120.0 : k == 3 ? -1.0 / 5040.0
-       : k == 4 ? 1.0 / 362880.0 : k == 5 ? -1.0 / 39916800.0 : k == 6 ? 1.0 / 6227020800.0
-       : k == 7 ? -1.0 / 1307674368000.0 : 1.0 / 355687428096000.0;
+__device__ __forceinline__ float sin_c(int k) {
+  return f32b(k == 0 ? 0x3F800000u : k == 1 ? 0xBE2AAAABu : k == 2 ? 0x3C088889u : k == 3 ? 0xB9500D01u : 0x3638EF1Du);
 }
-__host__ __device__ constexpr double cos_c(int k) {
-  return k == 0 ? 1.0 : k == 1 ? -1.0 / 2.0 : k == 2 ? 1.0 / 24.0 : k == 3 ? -1.0 / 720.0
-       : k == 4 ? 1.0 / 40320.0 : k == 5 ? -1.0 / 3628800.0 : k == 6 ? 1.0 / 479001600.0
-       : k == 7 ? -1.0 / 87178291200.0 : k == 8 ? 1.0 / 20922789888000.0
-       : -1.0 / 6402373705728000.0;
+__device__ __forceinline__ float cos_c(int k) {
+  return f32b(k == 0 ? 0x3F800000u : k == 1 ? 0xBF000000u : k == 2 ? 0x3D2AAAABu : k == 3 ? 0xBAB60B61u
+              : k == 4 ? 0x37D00D01u : 0xB493F27Eu);
 }
-
-// odd integer v = 2(x>>8)+1 in [1, 2^25); u = v * 2^-25
-__device__ __forceinline__ uint32_t odd25(uint32_t x) { return ((x >> 8) << 1) | 1u; }
-
-__device__ __forceinline__ double pow2i(int e) {  // exact 2^e for |e| < 1000
-  return __longlong_as_double((long long)(1023 + e) << 52);
-}
-
-// ln(u), u = ((x>>8)+0.5) 2^-24
-__device__ __forceinline__ double log_u(uint32_t x) {
-  const uint32_t v = odd25(x);
+// odd integer v = 2(x>>9)+1 in [1, 2^24); u = v * 2^-24 (exact in binary32)
+__device__ __forceinline__ uint32_t odd24(uint32_t x) { return ((x >> 9) << 1) | 1u; }
+// ln(u), u = (2(x>>9)+1) 2^-24: f = v 2^-e in [1, 2) (halved above sqrt 2), s = (f-1)/(f+1),
+// 2 s Horner(z = s^2), ln u = n LN2_HI + (n LN2_LO + lnf), n = e - 24; correctly rounded binary32
+// operations in the spec's order, never fused
+__device__ __forceinline__ float log_u(uint32_t x) {
+  const uint32_t v = odd24(x);
   int e = 31 - __clz(v);
-  double f = __dmul_rn((double)v, pow2i(-e));
-  if (f > kSqrt2) {
-    f = __dmul_rn(f, 0.5);
+  float f = __fmul_rn((float)v, __int_as_float((127 - e) << 23));   // exact: v < 2^24, 2^-e normal
+  if (f > f32b(kSqrt2)) {
+    f = __fmul_rn(f, 0.5f);
     e += 1;
   }
-  const double s = __ddiv_rn(__dadd_rn(f, -1.0), __dadd_rn(f, 1.0));
-  const double z = __dmul_rn(s, s);
-  double p = log_c(11);
+  const float s = __fdiv_rn(__fadd_rn(f, -1.0f), __fadd_rn(f, 1.0f));
+  const float z = __fmul_rn(s, s);
+  float p = log_c(4);
 #pragma unroll
-  for (int k = 10; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, z), log_c(k));
-  const double lnf = __dmul_rn(__dmul_rn(2.0, s), p);
-  const double n = (double)(e - 25);
-  return __dadd_rn(__dmul_rn(n, kLn2Hi), __dadd_rn(__dmul_rn(n, kLn2Lo), lnf));
+  for (int k = 3; k >= 0; --k) p = __fadd_rn(__fmul_rn(p, z), log_c(k));
+  const float lnf = __fmul_rn(__fmul_rn(2.0f, s), p);
+  const float n = (float)(e - 24);
+  return __fadd_rn(__fmul_rn(n, f32b(kLn2Hi)), __fadd_rn(__fmul_rn(n, f32b(kLn2Lo)), lnf));
 }
-
-// (sin, cos)(2 pi u)
-__device__ __forceinline__ void sincos_2pi_u(uint32_t x, double& so, double& co) {
-  const uint32_t w = odd25(x);
-  const uint32_t qd = w >> 23;
-  const uint32_t rem = w & ((1u << 23) - 1u);
-  const double t = __dmul_rn((double)rem, 0x1p-23);
-  const bool low = rem < (1u << 22);
-  const double xr = __dmul_rn(low ? t : __dadd_rn(1.0, -t), kPiO2);
-  const double y = __dmul_rn(xr, xr);
-  double ps = sin_c(8);
+// (sin, cos)(2 pi u): quadrant w >> 22, reduced t = (w mod 2^22) 2^-22, folded at 1/2
+__device__ __forceinline__ void sincos_2pi_u(uint32_t x, float& so, float& co) {
+  const uint32_t w = odd24(x);
+  const uint32_t qd = w >> 22;
+  const uint32_t rem = w & ((1u << 22) - 1u);
+  const float t = __fmul_rn((float)rem, 0x1p-22f);
+  const bool low = rem < (1u << 21);
+  const float xr = __fmul_rn(low ? t : __fadd_rn(1.0f, -t), f32b(kPiO2));
+  const float y = __fmul_rn(xr, xr);
+  float ps = sin_c(4);
 #pragma unroll
-  for (int k = 7; k >= 0; --k) ps = __dadd_rn(__dmul_rn(ps, y), sin_c(k));
-  const double sx = __dmul_rn(xr, ps);
-  double pc = cos_c(9);
+  for (int k = 3; k >= 0; --k) ps = __fadd_rn(__fmul_rn(ps, y), sin_c(k));
+  const float sx = __fmul_rn(xr, ps);
+  float pc = cos_c(5);
 #pragma unroll
-  for (int k = 8; k >= 0; --k) pc = __dadd_rn(__dmul_rn(pc, y), cos_c(k));
-  const double S = low ? sx : pc;
-  const double C = low ? pc : sx;
+  for (int k = 4; k >= 0; --k) pc = __fadd_rn(__fmul_rn(pc, y), cos_c(k));
+  const float S = low ? sx : pc;
+  const float C = low ? pc : sx;
   switch (qd) {
     case 0: so = S; co = C; break;
     case 1: so = C; co = -S; break;
@@ -105,15 +93,13 @@ __device__ __forceinline__ void sincos_2pi_u(uint32_t x, double& so, double& co)
     default: so = -C; co = S; break;
   }
 }
-
-// Box-Muller pair from (xa, xb) -> float32 (z0, z1)
+// Box-Muller pair from (xa, xb): (r cos, r sin), r = sqrt(-2 ln u_a), binary32
 __device__ __forceinline__ float2 box_muller(uint32_t xa, uint32_t xb) {
-  const double r = __dsqrt_rn(__dmul_rn(-2.0, log_u(xa)));
-  double s, c;
+  const float r = __fsqrt_rn(__fmul_rn(-2.0f, log_u(xa)));
+  float s, c;
   sincos_2pi_u(xb, s, c);
-  return make_float2(__double2float_rn(__dmul_rn(r, c)), __double2float_rn(__dmul_rn(r, s)));
+  return make_float2(__fmul_rn(r, c), __fmul_rn(r, s));
 }
-
 // Philox block for (seed, mode, row j, column quad c4): the 4 raw words
 __device__ __forceinline__ uint4 omega_bits(uint64_t seed, uint32_t mode, uint64_t j, uint32_t c4) {
   return philox4x32_10(make_uint4(c4, (uint32_t)j, (uint32_t)(j >> 32), mode),
@@ -133,7 +119,7 @@ __device__ __forceinline__ float unif_sym(uint32_t x) {
 }
 
 // Sketch columns (c2, c2 + 1) of row j (c2 even): from a materialised Omega_k ([m][l] row-major,
-// the Appendix D types, rtk_omega.cu) or RTK-GAUSS-1 generated in place (om == nullptr)
+// the Appendix D types, rtk_omega.cu) or RTK-GAUSS-2 generated in place (om == nullptr)
 __device__ __forceinline__ float2 sketch_pair(const float* om, int l, uint64_t seed, uint32_t mode, uint64_t j,
                                               int c2) {
   if (om) {

@@ -9,7 +9,7 @@
 //   RTK-KR-1    Omega_k(j, c) = fl32( prod_{m != k, ascending} F_m(i_m, c) ), product in binary64,
 //               j = sum_m i_m stride_m over the column modes (lower modes fastest);
 //               F_m (n_m x l) drawn like Omega with counter word 3 = 0x4B000000 | (m << 8) | k
-//               (Gaussian: RTK-GAUSS-1 pairs) or 0x4C000000 | (m << 8) | k (uniform: RTK-UNIF-1).
+//               (Gaussian: RTK-GAUSS-2 pairs) or 0x4C000000 | (m << 8) | k (uniform: RTK-UNIF-1).
 // The Gaussian Khatri-Rao factors are tiny (sum n_m l values), so the per-element cost is d - 1
 // table reads and products instead of a Philox block and a Box-Muller transform.
 #include <cuda_runtime.h>

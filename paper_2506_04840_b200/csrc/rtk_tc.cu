@@ -7,7 +7,7 @@
 //                         Epilogue writes W as tf32 hi/lo planes (the B operand of op2), or -- for
 //                         the ST shrink G x_k U_k^T -- the next unfolding.
 //   op2  Y += M W         (n x N, K = m, split-K over CTAs): A = M tile 128(i) x 32(j), MN-major
-//                         (4 TMA boxes {32,32}); B = W (or the RTK-GAUSS-1 sketch Omega_k, generated
+//                         (4 TMA boxes {32,32}); B = W (or the RTK-GAUSS-2 sketch Omega_k, generated
 //                         in shared memory: Y0 = M Omega_k, line 5) tile N(c) x 32(j), K-major;
 //                         D = all ceil(n/128) row tiles x N columns resident in TMEM; the per-CTA
 //                         partials go to the same fixed-order fp64 reduction as the FFMA path.
@@ -59,7 +59,7 @@ struct TcOp2Args {
   uint64_t seed;
   uint32_t mode;
   float* xmax;         // sketch: atomicMax of max|M| (the fp16 pair engine's scale, rtk_fused2.cu)
-  const float* om;   // materialised Omega_k [m][l] or nullptr (RTK-GAUSS-1 in place)
+  const float* om;   // materialised Omega_k [m][l] or nullptr (RTK-GAUSS-2 in place)
 };
 
 // ------------------------------------------------------------------ op1: W = M^T Q

@@ -3,7 +3,7 @@
 // One templated kernel streams the mode-k unfolding M (n x m) ONCE, column
 // block by column block, and per block J (b columns) computes
 //
-//   OP_SKETCH : W_J = Omega_k(J, :)                     (RTK-GAUSS-1, generated in SMEM)
+//   OP_SKETCH : W_J = Omega_k(J, :)                     (RTK-GAUSS-2, generated in SMEM)
 //               Y  += M_J W_J                           Alg. 3/4 line 5
 //   OP_POWER  : W_J = M_J^T Q                           Alg. 3/4 line 7
 //               Y  += M_J W_J                           -- fused single pass, M read once
@@ -45,7 +45,7 @@ struct TileArgs {
   int64_t yp_g;  // ltot * n_rows
   uint64_t seed;
   uint32_t mode;
-  const float* om;   // materialised Omega_k [m][l] (Appendix D types) or nullptr (RTK-GAUSS-1)
+  const float* om;   // materialised Omega_k [m][l] (Appendix D types) or nullptr (RTK-GAUSS-2)
   float* out;
   int64_t Rprev, nnext, ldnext;
 };
