@@ -38,9 +38,10 @@
  * RTK_ERR_NUMERIC no output is written.  rtk_last_error() returns a thread-local
  * message for the last non-zero status of this thread.
  *
- * NUMERIC FAILURES (RTK_ERR_NUMERIC).  A solve that meets a non-finite iterate or a
- * Cholesky breakdown its basis completion cannot repair still writes its outputs
- * (unreliable).  With a report (rep != NULL) that call returns RTK_ERR_NUMERIC and
+ * NUMERIC FAILURES (RTK_ERR_NUMERIC).  A solve that meets a non-finite iterate (a NaN /
+ * inf in A, or an iterate Y = M M^T Q beyond the fp32 range: the stream squares the
+ * scale of A, so max|A| must stay well below ~1e13) or a Cholesky breakdown its basis
+ * completion cannot repair still writes its outputs (unreliable).  With a report (rep != NULL) that call returns RTK_ERR_NUMERIC and
  * sets rep->numeric.  Without a report the call is asynchronous and cannot see its
  * own result: the failure is latched in a per-device flag and the NEXT solver call
  * on that device (once the failing solve has executed) returns RTK_ERR_NUMERIC

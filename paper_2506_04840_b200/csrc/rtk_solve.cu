@@ -1229,6 +1229,9 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   tck[ntck++] = clock64();
   cluster.sync();
   load_packed_sum(a.gsum, 1, 0, l, S.G);
+  // a non-finite iterate (non-finite input, or fp32 overflow of Y = M M^T Q) shows on the Gram's
+  // diagonal: report RTK_ERR_NUMERIC (the step still runs, its outputs are unreliable)
+  if (rank == 0 && tid < l && !isfinite(S.G[tid * kLD + tid])) a.status[0] = 6;
   tck[ntck++] = clock64();
 
   // ---- 2a. Alg. B.1 lines 9-12: all eigenvalues of G = Y^T Y give
@@ -1563,6 +1566,7 @@ __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
     for (int c = warp; c < a.r; c += kST / 32) {
       int bi = 0x7fffffff;
       for (int b = 0; b < C; ++b) bi = min(bi, (int)ldcg(amax2 + (int64_t)b * kSL + c));
+      if (bi < 0 || bi >= n) bi = 0;   // non-finite column (no maximum found): the numeric flag reports it
       const double sgn = ldcg(a.Qd + (int64_t)c * n + bi) < 0.0 ? -1.0 : 1.0;
       if (lane == 0) S.colscale[c] = sgn;
       for (int i = r0 + lane; i < r1; i += 32) a.U[(int64_t)c * n + i] = (float)(sgn * a.Qd[(int64_t)c * n + i]);

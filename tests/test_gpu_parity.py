@@ -610,3 +610,87 @@ def test_bitwise_repeatable_and_workspace_independent(dims, ranks, p, q, seq, mo
         else:
             for x, y in zip(ref, out):
                 assert torch.equal(x, y), it
+
+
+# ------------------------------------------------ the fp16 two-plane pair engine in the solver
+# (DESIGN.md 6.3).  Shapes whose power steps run on the pair engine: n_k > 256 and at least 37
+# pair-blocks of 256 columns; max|M| then comes from the sketch (pair or tcgen05) or the previous
+# mode's pair shrink.
+F16_SHAPES = [
+    ((700, 120, 100), (30, 10, 8), 10, 3),     # mode 1 on the pair engine (m = 12000), sketch by tc_op2
+    ((1000, 400, 30), (40, 30, 6), 8, 2),      # modes 1 and 2 (mode 2 after the pair shrink: m = 1200 -> one-CTA)
+    ((400, 300, 130), (20, 20, 10), 6, 2),     # mode 2 (n = 300, m = 20 * 130 = 2600 -> one-CTA), mode 1 pair
+]
+
+
+@pytest.mark.parametrize("dims,ranks,p,q", F16_SHAPES)
+def test_f16_engine_parity_and_agreement(dims, ranks, p, q, monkeypatch):
+    """Oracle parity with the fp16 engine, and agreement with the 3xTF32 engine (RTK_PAIR_F16=0) on
+    the same solve: both carry the same 22-bit operand split, so RE agrees to fp32 rounding and the
+    factors span the same subspaces."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import rsthosvd
+    rng = np.random.default_rng(sum(dims) + 7)
+    cr = tuple(min(n, r + 8) for n, r in zip(dims, ranks))
+    core = rng.standard_normal(cr) / np.sqrt(np.prod(np.indices(cr) + 1, axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    check(a, ranks, p, q, 77, True)
+    A = to_device_colmajor(a, torch)
+    out = {}
+    for f16 in ("1", "0"):
+        monkeypatch.setenv("RTK_PAIR_F16", f16)
+        core_g, U = rsthosvd(A, ranks, p, q, 77)
+        torch.cuda.synchronize()
+        out[f16] = (core_g.cpu().numpy(), [u.cpu().numpy() for u in U])
+    re1 = metrics.relative_error(a, *out["1"])
+    re0 = metrics.relative_error(a, *out["0"])
+    assert abs(re1 - re0) <= 1e-5 * re0, (re1, re0)
+    gaps = metrics.mode_gaps(a, ranks, out["0"][1], True)
+    for k, (u1, u0) in enumerate(zip(out["1"][1], out["0"][1])):
+        if gaps[k] > 0.10:
+            assert metrics.max_principal_angle(u0, u1) <= 1e-4, (k, gaps[k])
+
+
+@pytest.mark.parametrize("scale", [1e-15, 1e12])
+def test_f16_engine_extreme_tensor_scale(scale):
+    """The fp16 engine's power-of-two scales follow max|M| through the whole pipeline (sketch ->
+    power steps -> shrink -> next mode): a tensor scaled by 1e-15 / 1e12 gives the same relative
+    error and factors as the oracle (which is scale-invariant).  (The fp32 stream itself bounds the
+    range: Y = M M^T Q squares the scale, so max|A| ~ 3e13 already overflows fp32 in any engine;
+    test_non_finite_input_reports_numeric covers what happens then.)"""
+    c = CONFIGS["c5"]
+    a = make_config_tensor("c5", dims=(600, 200, 150)) * scale
+    check(a, (30, 20, 15), 8, 2, c["omega_seed"], True)
+
+
+def test_f16_engine_d4_after_pair_shrinks():
+    """d = 4 with the first two modes on the pair engine: mode 2's power steps take max|M| from mode
+    1's pair shrink (the unfolding the shrink wrote)."""
+    rng = np.random.default_rng(4242)
+    dims, ranks = (300, 280, 40, 30), (12, 10, 4, 3)   # mode 2: m = 12 * 40 * 30 = 14400 (56 pair-blocks)
+    cr = (16, 14, 6, 5)
+    core = rng.standard_normal(cr) * np.exp(-0.15 * np.indices(cr).sum(axis=0))
+    a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
+    check(a, ranks, 4, 2, 91, True)
+
+
+@pytest.mark.parametrize("bad", ["nan", "inf", "huge"])
+def test_non_finite_input_reports_numeric(bad):
+    """A non-finite input (or one whose power iterates overflow fp32) ends in RTK_ERR_NUMERIC from
+    the solve, never in a crash or an out-of-bounds access (the sign pin of a non-finite column)."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import RtkError, solve
+    a = make_config_tensor("c5", dims=(600, 200, 150))
+    if bad == "nan":
+        a[3, 4, 5] = np.nan
+    elif bad == "inf":
+        a[0, 0, 0] = np.inf
+    else:
+        a = a * 1e15
+    A = to_device_colmajor(a, torch)
+    with pytest.raises(RtkError) as ei:
+        solve(A, (30, 20, 15), 8, 2, 5002, sequential=True, report=True)
+    assert "NUMERIC" in str(ei.value)
+    # the next solve on the same device runs normally
+    b = make_config_tensor("c1")
+    solve(to_device_colmajor(b, torch), (5, 5, 5), 5, 2, 1002, sequential=True, report=True)
