@@ -3,7 +3,7 @@
 // After a streaming kernel has produced per-CTA fp32 partial sums of M (M^T Q) (or M Omega_k),
 // one step of Alg. 3/4 finishes in TWO launches:
 //
-//   reduce_gram_kernel  (whole GPU, 8 rows per CTA)
+//   reduce_gram_kernel  (whole GPU, 8 rows per CTA, 512 threads)
 //       Y = sum_g Ypart[g] - alpha Q           fixed g order, fp64 (Alg. 3/4 line 7's "- alpha Q")
 //       per-block packed upper Gram  Y_b^T Y_b
 //   step_kernel         (one thread-block cluster of C <= 8 CTAs, 256 threads each)
@@ -47,7 +47,11 @@ constexpr int kLD = 65;        // leading dimension of the l x l fp64 shared mat
 constexpr int kMLD = 66;       // leading dimension of T (even: 16-byte double2 rows)
 constexpr int kST = 256;       // threads per CTA
 constexpr int kRBr = 8;        // rows per reduce_gram CTA
-constexpr int kRGC = 8;        // reduce_gram cluster: one Gram partial per kRGC * kRBr = 64 rows
+#ifndef RTK_RGC
+#define RTK_RGC 4
+#endif
+constexpr int kRGC = RTK_RGC;   // reduce_gram cluster: one Gram partial per kRGC * kRBr = 32 rows (8-CTA clusters
+                                // launch ~8 us slower: C5 reduce 22 -> 14.5 us, solve 9.60 -> 9.42 ms)
 constexpr int kChunk = 64;     // rows per product chunk in step_kernel
 constexpr int kMaxC = 16;      // cluster size (16: non-portable opt-in, checked by occupancy query)
 constexpr double kPinTie = 1e-5;   // sign pin: |entries| within this (relative) of the max are tied (C6)
@@ -61,11 +65,13 @@ __device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
 }
 
 // =============================================================== reduce + Gram partials
-// Gram partials: one per 64-row block (a cluster of kRGC CTAs sums its CTAs' 8-row Grams through
-// distributed shared memory), so the consumers sum ceil(n / 64) partials, not ceil(n / 8).
+// Gram partials: one per 32-row block (a cluster of kRGC CTAs sums its CTAs' 8-row Grams through
+// distributed shared memory), so the consumers sum ceil(n / 32) partials, not ceil(n / 8).
 __host__ __device__ constexpr int gram_blocks(int n) { return (n + kRGC * kRBr - 1) / (kRGC * kRBr); }
 
-__global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restrict__ Ypart, int G, int ltot,
+constexpr int kRT = 512;   // reduce_gram threads: (column c = tid / 8, partial slice h = tid % 8)
+
+__global__ void __launch_bounds__(kRT) reduce_gram_kernel(const float* __restrict__ Ypart, int G, int ltot,
                                                          int n_rows, int n, int l,
                                                          const double* __restrict__ Qd,
                                                          const double* __restrict__ alpha, int power,
@@ -74,7 +80,6 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
   // gmode 0: Y and the Gram partials; 1: Y only (a multi-GPU shard, before Y's all-reduce);
   // 2: the Gram partials of the (all-reduced) Y already in Y
   __shared__ double Ys[kRBr][kSL + 1];
-  __shared__ double red[4][kSL][kRBr];
   __shared__ double gps[kSL * (kSL + 1) / 2];   // this CTA's 8-row Gram (packed upper)
   sm100::pdl_wait();   // the power step's Y partials
   if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode (uniform over the grid)
@@ -83,38 +88,43 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
   const int rows = min(kRBr, n - i0);
   const double a = power ? *alpha : 0.0;
   const int64_t gs = (int64_t)ltot * n_rows;
-  static_assert(kRBr == 8 && kST == 4 * kSL, "thread (column c, partial slice h) layout");
-  if (gmode != 2) {   // thread (c, h) sums the partials g = h, h+4, ... of its column's 8 rows: two 16-B loads
-      // per partial, all independent (the rows past n are Ypart padding, masked below; n_rows is a
-      // multiple of 4, and a last group with only 4 rows inside n_rows takes the scalar loop)
-    const int c = tid % kSL, h = tid / kSL;
+  static_assert(kRBr == 8 && kRT == 8 * kSL, "thread (column c, partial slice h) layout");
+  // thread (c, h) sums the partials g = h, h+8, ... of its column's 8 rows (two 16-B loads per
+  // partial, five partials in flight: ~150 KB of partials in flight per CTA); the 8 slices of a
+  // column are 8 consecutive lanes and meet in a fixed xor tree (repeatable results).  The rows past n
+  // are Ypart padding, masked below; n_rows is a multiple of 4, and a last group with only 4 rows
+  // inside n_rows takes the scalar loop.
+  const int c = tid >> 3, h = tid & 7;
+  for (int ii = tid; ii < kRBr * (kSL + 1); ii += kRT) Ys[ii / (kSL + 1)][ii % (kSL + 1)] = 0.0;
+  __syncthreads();
+  if (gmode != 2) {
     double acc[kRBr];
 #pragma unroll
     for (int ii = 0; ii < kRBr; ++ii) acc[ii] = 0.0;
     if (c < l && i0 + kRBr > n_rows) {
       const float* src = Ypart + (int64_t)c * n_rows + i0;
-      for (int g = h; g < G; g += 4)
+      for (int g = h; g < G; g += 8)
         for (int ii = 0; ii < n_rows - i0; ++ii) acc[ii] += (double)__ldcg(src + (int64_t)g * gs + ii);
     } else if (c < l) {
       const float* src = Ypart + (int64_t)c * n_rows + i0;
       int g = h;
-      for (; g + 12 < G; g += 16) {   // 4 partials of this slice in flight
-        float4 v[8];
+      for (; g + 32 < G; g += 40) {
+        float4 v[10];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4* p = reinterpret_cast<const float4*>(src + (int64_t)(g + 4 * u) * gs);
+        for (int u = 0; u < 5; ++u) {
+          const float4* p = reinterpret_cast<const float4*>(src + (int64_t)(g + 8 * u) * gs);
           v[2 * u] = __ldcg(p);
           v[2 * u + 1] = __ldcg(p + 1);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 5; ++u) {
           acc[0] += (double)v[2 * u].x; acc[1] += (double)v[2 * u].y;
           acc[2] += (double)v[2 * u].z; acc[3] += (double)v[2 * u].w;
           acc[4] += (double)v[2 * u + 1].x; acc[5] += (double)v[2 * u + 1].y;
           acc[6] += (double)v[2 * u + 1].z; acc[7] += (double)v[2 * u + 1].w;
         }
       }
-      for (; g < G; g += 4) {
+      for (; g < G; g += 8) {
         const float4* p = reinterpret_cast<const float4*>(src + (int64_t)g * gs);
         const float4 x = __ldcg(p), y = __ldcg(p + 1);
         acc[0] += (double)x.x; acc[1] += (double)x.y; acc[2] += (double)x.z; acc[3] += (double)x.w;
@@ -122,28 +132,26 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
       }
     }
 #pragma unroll
-    for (int ii = 0; ii < kRBr; ++ii) red[h][c][ii] = acc[ii];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kRBr * l; idx += kST) {
-    const int c = idx / kRBr, ii = idx % kRBr;
-    double s = 0.0;
-    if (ii < rows) {   // the four slices in a fixed order: repeatable results
-      const int i = i0 + ii;
-      if (gmode == 2) {
-        s = Y[(int64_t)c * n + i];
-      } else {
-        s = ((red[0][c][ii] + red[1][c][ii]) + red[2][c][ii]) + red[3][c][ii];
-        if (power) s -= a * Qd[(int64_t)c * n + i];
-        Y[(int64_t)c * n + i] = s;
-      }
+    for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+      for (int ii = 0; ii < kRBr; ++ii) acc[ii] += __shfl_xor_sync(0xffffffffu, acc[ii], o);
+    // lane h of the column group finishes row h: Y = sum - alpha Q
+    double sh = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < kRBr; ++ii) sh = (ii == h) ? acc[ii] : sh;
+    if (c < l && h < rows) {
+      const int i = i0 + h;
+      if (power) sh -= a * Qd[(int64_t)c * n + i];
+      Y[(int64_t)c * n + i] = sh;
+      Ys[h][c] = sh;
     }
-    Ys[ii][c] = s;
+  } else if (c < l && h < rows) {
+    Ys[h][c] = Y[(int64_t)c * n + i0 + h];
   }
   if (gmode == 1) return;   // uniform over the grid: before any cluster barrier
   __syncthreads();
   const int np = l * (l + 1) / 2;
-  for (int e = tid; e < np; e += kST) {
+  for (int e = tid; e < np; e += kRT) {
     int c1, c2;
     unpack_upper(e, c1, c2);
     double s = 0.0;
@@ -151,14 +159,14 @@ __global__ void __launch_bounds__(kST) reduce_gram_kernel(const float* __restric
     for (int ii = 0; ii < kRBr; ++ii) s += Ys[ii][c1] * Ys[ii][c2];
     gps[e] = s;
   }
-  // the cluster's 64-row partial: CTA r sums its share of the entries over the kRGC CTAs' Grams
+  // the cluster's 32-row partial: CTA r sums its share of the entries over the kRGC CTAs' Grams
   // (CTA order), read through distributed shared memory
   cg::cluster_group cluster = cg::this_cluster();
   cluster.sync();
   const int r = (int)cluster.block_rank();
   double* gp = gpart + (int64_t)(blockIdx.x / kRGC) * np;
   const int e0 = r * np / kRGC, e1 = (r + 1) * np / kRGC;
-  for (int e = e0 + tid; e < e1; e += kST) {
+  for (int e = e0 + tid; e < e1; e += kRT) {
     double v[kRGC];
 #pragma unroll
     for (int q = 0; q < kRGC; ++q) v[q] = cluster.map_shared_rank(gps, q)[e];
@@ -1957,7 +1965,7 @@ size_t solve_gpart_doubles(int n, int l) { return (size_t)gram_blocks(n) * l * (
 cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop, int gmode) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(gram_blocks(B.n) * kRGC, 1, 1);   // CTAs past n contribute zero rows
-  cfg.blockDim = dim3(kST, 1, 1);
+  cfg.blockDim = dim3(kRT, 1, 1);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1968,6 +1976,10 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  if (kRGC == 1) {   // no cluster: the PDL attribute alone
+    attr[0] = attr[1];
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, reduce_gram_kernel, (const float*)B.Ypart, B.G, B.ltot, B.n_rows, B.n,
                                      B.l, (const double*)B.Qd, (const double*)B.alpha, power ? 1 : 0, B.Y, B.gpart,
                                      stop, gmode);
