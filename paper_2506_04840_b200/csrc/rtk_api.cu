@@ -873,16 +873,19 @@ int solve_shard(const rtk_options& o, const float* A, const int64_t* dims, int32
   // the report slots sit at the same offsets in both layouts (they depend on d and q only)
   RTK_CK(cudaMemsetAsync(ws + Lf.status, 0, (size_t)d * 4 * 4, st));
   RTK_CK(cudaMemsetAsync(ws + Lf.trace, 0, (size_t)d * q * 8, st));
+  RTK_CK(cudaMemsetAsync(ws + Ll.xmax, 0, 8 * 4, st));   // same offset in both layouts (d, q only)
+  XState xs_slab;   // fp16 pair engine on the slab: each rank scales by its own slab's max|M|
+  xs_slab.xmax = (float*)(ws + Ll.xmax);
   const bool shift = o.shift != 0;
   float* shr[2] = {(float*)(ws + Ll.shr0), (float*)(ws + Ll.shr1)};
   // modes 1 .. d-1 on the slab; the last shrink leaves the slab's mode-d unfolding in shr[(d-2)&1]
   for (int k = 0; k + 1 < d; ++k) {
     const float* cur = k == 0 ? A : shr[(k - 1) & 1];
     const View rv = range_view(S.loc, k, A, cur);
-    rc = run_mode(S.loc, Ll, ws, k, rv, seed, shift, U[k], st);
+    rc = run_mode(S.loc, Ll, ws, k, rv, seed, shift, U[k], st, &xs_slab);
     if (rc) return rc;
     const View sv = shrink_view(S.loc, k, A, cur);
-    rc = run_shrink(S.loc, Ll, ws, k, sv, U[k], shr[k & 1], st);
+    rc = run_shrink(S.loc, Ll, ws, k, sv, U[k], shr[k & 1], st, &xs_slab);
     if (rc) return rc;
   }
   // gather: the slab's rows [last_begin, +last_count) of the mode-d unfolding, zero elsewhere, summed
@@ -897,7 +900,11 @@ int solve_shard(const rtk_options& o, const float* A, const int64_t* dims, int32
   {
     const int k = d - 1;
     const View rv = range_view(S.full, k, A, full);
-    rc = run_mode(S.full, Lf, ws, k, rv, seed, shift, U[k], st);
+    // the gathered unfolding's max|M| is known only once its own sketch has run (the slab's shrink
+    // saw one rank's rows; its atomicMax is a lower bound the sketch's raises to the full maximum)
+    XState xs_full;
+    xs_full.xmax = (float*)(ws + Lf.xmax);
+    rc = run_mode(S.full, Lf, ws, k, rv, seed, shift, U[k], st, &xs_full);
     if (rc) return rc;
     const View sv = shrink_view(S.full, k, A, full);
     rc = run_shrink(S.full, Lf, ws, k, sv, U[k], core, st);

@@ -1004,7 +1004,7 @@ cudaError_t pair_power(const View& v, int l, const float* planes, int pld, float
   PairArgs a;
   a.n = v.n; a.m = m; a.nt = nt; a.nk1 = (v.n + KS - 1) / KS; a.nblk = nblk;
   a.Ypart = Ypart; a.stop = stop;
-  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : (H ? 2 : 8);   // stages (H: 64 rows each; 0-4 within 3 %, ncu)
+  a.lag = getenv("RTK_PAIR_LAG") ? atoi(getenv("RTK_PAIR_LAG")) : (H ? 1 : 8);   // stages (H: 64 rows each; lag 1 fastest of 0-4, DRAM 4.23 GB)
   a.dbg = getenv("RTK_PAIR_DBG") ? atoi(getenv("RTK_PAIR_DBG")) : 0;
   a.shrink = shrink_out ? 1 : 0;
   a.out = shrink_out;

@@ -179,7 +179,8 @@ def _gpu_worker(rank, world, port, dims, ranks, p, q, out, kind=0):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dims,ranks,p,q", [
-    ((1000, 64, 40), (50, 10, 8), 10, 3),    # mode 1 on the pair engine (n > 256), l = 60
+    ((1000, 64, 40), (50, 10, 8), 10, 3),    # mode 1 on the one-CTA engine (5 pair-blocks per slab), l = 60
+    ((1000, 200, 100), (30, 10, 8), 6, 2),   # mode 1 on the fp16 pair engine (39 pair-blocks per slab)
     ((120, 90, 33), (12, 9, 6), 5, 2),       # one-CTA engine, odd slab extents (17 + 16)
     ((40, 30, 20, 18), (6, 5, 4, 3), 4, 2),  # d = 4
 ])
