@@ -694,3 +694,26 @@ def test_non_finite_input_reports_numeric(bad):
     # the next solve on the same device runs normally
     b = make_config_tensor("c1")
     solve(to_device_colmajor(b, torch), (5, 5, 5), 5, 2, 1002, sequential=True, report=True)
+
+
+def test_f16_engine_zero_and_exact_low_rank():
+    """On the fp16 pair engine (n_1 = 400 > 256, 40 pair-blocks): an all-zero tensor (max|M| = 0, the
+    scale clamps) gives a finite orthonormal basis and a zero core; an exactly rank-(6, 5, 4) Tucker
+    tensor is recovered to fp32 rounding (RE < 1e-5) with l > rank (basis completion)."""
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import solve
+    dims = (400, 128, 80)
+    A = to_device_colmajor(np.zeros(dims, dtype=np.float32), torch)
+    core, U, rep = solve(A, (20, 10, 8), 6, 2, 5, sequential=True, report=True)
+    torch.cuda.synchronize()
+    assert rep.numeric == 0
+    assert torch.count_nonzero(core).item() == 0
+    for u in U:
+        un = u.cpu().numpy()
+        assert np.all(np.isfinite(un)) and metrics.orthonormality(un) <= ORTH_TOL
+    rng = np.random.default_rng(11)
+    ranks = (6, 5, 4)
+    a = tucker_tensor(rng.standard_normal(ranks), [orthonormal_factor(n, r, rng) for n, r in zip(dims, ranks)])
+    g_core, g_U, rep = solve(to_device_colmajor(a, torch), (10, 8, 6), 6, 2, 5, sequential=True, report=True)
+    re = metrics.relative_error(a, g_core.cpu().numpy(), [u.cpu().numpy() for u in g_U])
+    assert re < 1e-5, re
