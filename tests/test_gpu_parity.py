@@ -282,6 +282,7 @@ def _pve_ratios(tr, r):
     ((60, 50, 40), (6, 5, 4), 4, 8, 3e-2),     # stops in between
     ((700, 30, 24), (12, 6, 5), 6, 8, 1e-2),   # n_1 > 512 (2-CTA fused cluster)
     ((45, 40, 36, 30), (5, 4, 4, 3), 3, 7, 5e-2),
+    ((600, 120, 90), (20, 8, 6), 6, 8, 1e-2),  # mode 1 on the fp16 pair engine (42 pair-blocks)
 ])
 def test_pve_parity(path, dims, ranks, p, qmax, tol, monkeypatch):
     """Alg. B.1 on the GPU vs the oracle: the same stop step per mode, the same alpha trace up
