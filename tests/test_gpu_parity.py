@@ -403,6 +403,7 @@ def test_a2_config_parity(cfg, path, monkeypatch):
 @pytest.mark.parametrize("shift", [True, False])
 @pytest.mark.parametrize("dims,ranks,p,q", [
     ((640, 40, 36), (20, 8, 6), 6, 3),        # n_1 > 512: 2-CTA fused cluster
+    ((500, 160, 70), (16, 8, 6), 6, 2),       # mode 1 on the fp16 pair engine (44 pair-blocks)
     ((37, 29, 23), (4, 5, 3), 3, 2),          # odd sizes, ragged tiles
     ((16, 12, 10, 9), (3, 2, 4, 2), 2, 3),    # d = 4
     ((40, 30), (6, 4), 2, 2),                 # d = 2
