@@ -220,7 +220,7 @@ struct Layout {
   std::vector<char> tc_range, tc_shrink;
   size_t ypart = 0, y = 0, q1 = 0, qd = 0, qs = 0, gpart = 0, T = 0, lam = 0;
   size_t alpha = 0, trace = 0, sigma = 0, status = 0, sighat = 0, shr0 = 0, shr1 = 0, total = 0;
-  size_t g2part = 0, gsum = 0, amax = 0, lamx = 0;
+  size_t g2part = 0, gsum = 0, amax = 0, lamx = 0, gbar = 0;
   size_t xmax = 0;   // [8] floats: max|M| of each mode's unfolding (the fp16 pair engine's scale)
   size_t a2q = 0, a2b = 0, a2g0 = 0, a2g1 = 0, a2gram = 0, a2v = 0;   // Alg. A.2 only
   size_t om = 0, omtab = 0;                                         // Appendix D sketches only
@@ -326,6 +326,7 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
   L.amax = take((size_t)16 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 16 CTAs
   L.lamx = take((size_t)kSolveLMax * 8);            // eigenvalues shared across the step cluster
+  L.gbar = take(16);                                 // the step kernel's grid barrier
   if (P.omega || P.full_last) {   // materialised Omega_k (Appendix D types; every type on a shard)
     size_t oms = 0, tabs = 0;
     for (int k = 0; k < P.d; ++k) {
@@ -458,8 +459,10 @@ int run_mode(const Problem& P, const Layout& L, char* ws, int k, const View& v, 
   B.gsum = (double*)(mw + L.gsum);
   B.amax = (double*)(mw + L.amax);
   B.lamx = (double*)(mw + L.lamx);
+  B.gbar = (unsigned int*)(mw + L.gbar);
   const bool fast = l <= kSolveLMax;   // cluster small solver (rtk_solve.cu)
   RTK_CK(cudaMemsetAsync(B.alpha, 0, sizeof(double), st));   // alpha = 0 (line 5)
+  RTK_CK(cudaMemsetAsync(B.gbar, 0, 16, st));                 // step-kernel grid barrier
   const uint32_t mode1 = (uint32_t)(k + 1);
   const bool strided = v.P > 1;
   const bool tc = L.tc_range[k] && (strided ? (fast && fused_ok(v, l)) : tc_supported(v, l));

@@ -78,6 +78,7 @@ struct ModeBufs {
   double* gsum = nullptr;   // [np]
   double* amax = nullptr;   // [8][128] sign-pin argmax exchange
   double* lamx = nullptr;   // [64] eigenvalues exchanged across the cluster (final / B.1 steps)
+  unsigned int* gbar = nullptr;   // [2] step-kernel grid barrier (zeroed at mode start)
 };
 
 cudaError_t launch_reduce_gram(const ModeBufs& B, bool power, cudaStream_t st);

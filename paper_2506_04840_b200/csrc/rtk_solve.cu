@@ -886,9 +886,40 @@ __device__ __noinline__ void all_eigs(const double* d, const double* e, const do
 // of the 4-thread 5-section in all_eigs), same convergence rule as all_eigs; each eigenvalue is
 // computed by exactly one CTA (deterministic) and published to lamx, then every CTA reads all l
 // after a cluster barrier.  lam[c] = c-th smallest.  cnt: kST ints, blo / bhi: kSL doubles.
+// The step kernel's CTAs exchange data only through global memory (L2, ld.global.cg) and need a
+// barrier with release / acquire ordering between them: a cluster barrier, or (gbar != nullptr) a
+// self-resetting grid barrier in global memory -- a plain 16-CTA grid launches faster than a 16-CTA
+// cluster (non-portable size).  gbar[0] counts arrivals, gbar[1] is the generation; both start at
+// zero (memset per mode) and the count returns to zero after every barrier.  The CTAs are co-resident
+// in practice (<= 16 CTAs; waiting CTAs only wait for the stream predecessor's CTAs to drain).
+struct StepSync {
+  unsigned int* gbar;
+  __device__ void sync() const {
+    if (!gbar) {
+      cg::this_cluster().sync();
+      return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      volatile unsigned int* vgen = gbar + 1;
+      const unsigned int gen = *vgen;   // before arriving: the last arrival bumps it
+      __threadfence();                  // release this CTA's global writes
+      if (atomicAdd(gbar, 1u) == gridDim.x - 1) {
+        *(volatile unsigned int*)gbar = 0u;
+        __threadfence();
+        atomicAdd(gbar + 1, 1u);
+      } else {
+        while (*vgen == gen) { }
+      }
+      __threadfence();                  // acquire the other CTAs' writes
+    }
+    __syncthreads();
+  }
+};
+
 __device__ __noinline__ void all_eigs_cluster(const double* d, const double* e, const double* e2, int l, double* lam,
                                  double* blo, double* bhi, int* cnt, double* lamx, int rank, int C,
-                                 cg::cluster_group& cluster) {
+                                 const StepSync& cluster) {
   const int tid = threadIdx.x;
   __shared__ double s_gl, s_gu;
   if (tid == 0) {
@@ -1050,6 +1081,7 @@ struct StepArgs {
   int pN, pld;
   int planes16;             // planes are the fp16 engine's: __half [2 pN][pld], Q scaled by 2^15
   int chol_old;             // RTK_CHOL=0: the 4 x 4 Cholesky + substitution inverse (A/B only)
+  unsigned int* gbar;       // grid barrier (nullptr: a thread-block cluster, RTK_STEP_GBAR=0)
   int chol_prof;            // RTK_CHOL=2: phase clocks of chol_inv into g_chol_prof
   double* alpha;
   double* trace;            // [q]
@@ -1198,9 +1230,9 @@ __device__ void load_packed_sum(const double* src, int parts, int64_t stride, in
 __global__ void __launch_bounds__(kST, 1) step_kernel(const StepArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   StepSmem& S = *reinterpret_cast<StepSmem*>(smraw);
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
+  const StepSync cluster{a.gbar};
+  const int C = a.gbar ? (int)gridDim.x : (int)cg::this_cluster().num_blocks();
+  const int rank = a.gbar ? (int)blockIdx.x : (int)cg::this_cluster().block_rank();
   const int tid = threadIdx.x;
   const int n = a.n, l = a.l;
   const int np = l * (l + 1) / 2;
@@ -2022,6 +2054,11 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   a.pin_q = pin_q ? 1 : 0;
   a.lamx = B.lamx;
   const int C = solve_cluster_size(B.n);
+  // the grid barrier for the non-portable 16-CTA size (C5: 9.39 -> 9.31 ms); up to 8 CTAs the cluster
+  // barrier is cheaper (C4, 2 CTAs: 1.85 vs 1.90 ms).  RTK_STEP_GBAR=0 / 1 forces either.
+  const char* gb = getenv("RTK_STEP_GBAR");
+  const bool use_gbar = gb ? gb[0] != '0' : C > 8;
+  a.gbar = (B.gbar && use_gbar) ? B.gbar : nullptr;
   const size_t smem = sizeof(StepSmem);
   cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -2039,6 +2076,10 @@ cudaError_t launch_step(const ModeBufs& B, int step, int q, bool shift, float* U
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  if (a.gbar) {   // plain grid, software barrier: the PDL attribute alone
+    attr[0] = attr[1];
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  }
   e = cudaLaunchKernelEx(&cfg, step_kernel, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
