@@ -322,9 +322,9 @@ Layout plan(const Problem& P, int nsm, const float* A, int path) {
   L.T = take(ll * 8);
   L.lam = take(lmax * 8);
   L.sighat = take(lmax * 8);
-  L.g2part = take((size_t)16 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);   // <= 16 cluster CTAs
+  L.g2part = take((size_t)32 * kSolveLMax * (kSolveLMax + 1) / 2 * 8);   // <= 32 step-kernel CTAs
   L.gsum = take((size_t)kSolveLMax * (kSolveLMax + 1) / 2 * 8);
-  L.amax = take((size_t)16 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 16 CTAs
+  L.amax = take((size_t)32 * 3 * kSolveLMax * 8);   // (max, index) pairs + the tie-pivot indices, <= 32 CTAs
   L.lamx = take((size_t)kSolveLMax * 8);            // eigenvalues shared across the step cluster
   L.gbar = take(16);                                 // the step kernel's grid barrier
   if (P.omega || P.full_last) {   // materialised Omega_k (Appendix D types; every type on a shard)

@@ -53,7 +53,7 @@ constexpr int kRBr = 8;        // rows per reduce_gram CTA
 constexpr int kRGC = RTK_RGC;   // reduce_gram cluster: one Gram partial per kRGC * kRBr = 32 rows (8-CTA clusters
                                 // launch ~8 us slower: C5 reduce 22 -> 14.5 us, solve 9.60 -> 9.42 ms)
 constexpr int kChunk = 64;     // rows per product chunk in step_kernel
-constexpr int kMaxC = 16;      // cluster size (16: non-portable opt-in, checked by occupancy query)
+constexpr int kMaxC = 32;      // step-kernel CTAs (a cluster up to 8 / 16 (non-portable); beyond 8 the grid barrier)
 constexpr double kPinTie = 1e-5;   // sign pin: |entries| within this (relative) of the max are tied (C6)
 
 __device__ __forceinline__ void unpack_upper(int e, int& c1, int& c2) {
@@ -1987,9 +1987,15 @@ static int max_step_cluster() {
 }
 
 int solve_cluster_size(int n) {
-  int C = (n + kChunk - 1) / kChunk;
-  if (C > 8) C = std::min(C, max_step_cluster());
-  return std::max(1, std::min(kMaxC, C));
+  const int C = (n + kChunk - 1) / kChunk;
+  if (C <= 8) return std::max(1, C);
+  // more than 8 CTAs run on the grid barrier (no cluster size limit) unless RTK_STEP_GBAR=0;
+  // RTK_STEP_ROWS sets the rows per CTA there (A/B timing)
+  const char* gb = getenv("RTK_STEP_GBAR");
+  if (gb && gb[0] == '0') return std::min(C, max_step_cluster());
+  const char* sr = getenv("RTK_STEP_ROWS");
+  const int rows = sr ? std::max(16, atoi(sr)) : kChunk;
+  return std::max(1, std::min(kMaxC, (n + rows - 1) / rows));
 }
 
 size_t solve_gpart_doubles(int n, int l) { return (size_t)gram_blocks(n) * l * (l + 1) / 2; }
