@@ -5,6 +5,7 @@
 // rtk_small.cu.  Nothing is copied back to the host during a solve (alpha lives in
 // device memory), so the sequence is stream-ordered and CUDA-graph capturable.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -925,6 +926,130 @@ int solve_shard(const rtk_options& o, const float* A, const int64_t* dims, int32
   return RTK_OK;
 }
 
+// ---------------------------------------------------------------- CUDA-graph replay of a solve
+// A solve is ~100-300 launches (PDL chains, side-stream forks, memsets) whose host enqueue and
+// launch gaps cost up to ~3 % of a small config (C4).  Repeated calls with IDENTICAL arguments
+// (every pointer, extent, option, the seed, the device and every RTK_* environment override) replay
+// one captured graph instead: the first call of a key runs directly (it also creates the lazily
+// allocated streams / events / pinned flags), the second captures the enqueue on a private stream
+// (relaxed capture mode) and launches the graph on the caller's stream, later calls only launch.
+// Replay reads and writes the same buffers through the same kernels, so results are bit-identical
+// to the direct path (tests/test_gpu_graph.py).  Bypassed when a report is requested (it needs a
+// host sync), when the library allocates the workspace, while per-launch profiling or the step-clock
+// diagnostics are active, when the caller's stream is itself capturing, and with RTK_GRAPH=0.
+// The sticky RTK_ERR_NUMERIC check runs on the host before every replay, as on the direct path.
+struct GraphEntry {
+  std::string key;
+  int seen = 0;                 // direct runs of this key so far
+  bool bad = false;             // capture failed once: always direct
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;       // kernel launches the captured enqueue counted
+};
+
+std::string graph_key(const rtk_options& o, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+                      int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
+                      int dev) {
+  std::string key;
+  key.reserve(512);
+  auto add = [&](unsigned long long x) { key += std::to_string(x); key += ','; };
+  add((unsigned)dev); add((unsigned)o.sequential); add((unsigned)o.shift); add((unsigned)o.path);
+  add((unsigned)o.variant); add((unsigned)o.omega);
+  unsigned long long pb = 0;
+  std::memcpy(&pb, &o.pve_tol, sizeof(pb));
+  add(pb);
+  add((uintptr_t)A); add((unsigned)d); add((unsigned)p); add((unsigned)q); add(seed);
+  for (int k = 0; k < d; ++k) { add((unsigned long long)dims[k]); add((unsigned)ranks[k]); add((uintptr_t)U[k]); }
+  add((uintptr_t)core); add((uintptr_t)ws); add(ws_bytes);
+  // every RTK_* override (path and engine switches are read at enqueue time)
+  for (char** e = ::environ; e && *e; ++e)
+    if (std::strncmp(*e, "RTK_", 4) == 0) { key += *e; key += ';'; }
+  return key;
+}
+
+bool graph_enabled() {
+  const char* g = getenv("RTK_GRAPH");
+  return !(g && g[0] == '0');
+}
+
+int solve_entry(const rtk_options& o, const float* A, const int64_t* dims, int32_t d, const int32_t* ranks,
+                int32_t p, int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
+                void* stream, rtk_report* rep) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (rep || !ws || g_prof_on.load() || g_step_dbg || !graph_enabled() || !A || !dims || !ranks || !U || !core ||
+      d < 2 || d > 8 || cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+  }
+  int dev = 0;
+  RTK_CK(cudaGetDevice(&dev));
+  const std::string key = graph_key(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, dev);
+  static std::mutex mu;
+  static std::vector<GraphEntry> cache;   // most recently used last
+  std::unique_lock<std::mutex> lk(mu);
+  size_t idx = cache.size();
+  for (size_t i = 0; i < cache.size(); ++i)
+    if (cache[i].key == key) { idx = i; break; }
+  if (idx == cache.size()) {
+    if (cache.size() >= 16) {   // evict the least recently used graph (no launch of it may be pending)
+      if (cache.front().exec) {
+        cudaDeviceSynchronize();
+        cudaGraphExecDestroy(cache.front().exec);
+      }
+      cache.erase(cache.begin());
+    }
+    GraphEntry e;
+    e.key = key;
+    cache.push_back(std::move(e));
+    idx = cache.size() - 1;
+  } else if (idx + 1 != cache.size()) {
+    std::rotate(cache.begin() + idx, cache.begin() + idx + 1, cache.end());
+    idx = cache.size() - 1;
+  }
+  GraphEntry& E = cache[idx];
+  if (!E.exec && (E.bad || E.seen == 0)) {   // first sight (or uncapturable): direct
+    lk.unlock();
+    const int rc = solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+    lk.lock();
+    for (auto& c : cache)
+      if (c.key == key && rc == RTK_OK) c.seen += 1;
+    return rc;
+  }
+  if (!E.exec) {   // second sight: capture the enqueue on a private stream
+    static thread_local cudaStream_t cs[64] = {};
+    if (dev < 0 || dev >= 64) return solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+    if (!cs[dev]) RTK_CK(cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking));
+    const long long l0 = g_launches.load();
+    RTK_CK(cudaStreamBeginCapture(cs[dev], cudaStreamCaptureModeRelaxed));
+    const int rc = solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, (void*)cs[dev], nullptr);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs[dev], &g);
+    cudaGraphExec_t ex = nullptr;
+    cudaError_t ei = cudaErrorUnknown;
+    if (rc == RTK_OK && ec == cudaSuccess && g) ei = cudaGraphInstantiate(&ex, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (rc != RTK_OK) return rc;   // argument / numeric errors: nothing was enqueued
+    if (ec != cudaSuccess || ei != cudaSuccess) {   // not capturable: direct from now on
+      cudaGetLastError();
+      if (ex) cudaGraphExecDestroy(ex);
+      E.bad = true;
+      lk.unlock();
+      return solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+    }
+    E.exec = ex;
+    E.launches = g_launches.load() - l0;
+  }
+  int* nflag = numeric_flag_host(dev);
+  if (nflag && *(volatile int*)nflag) {
+    *(volatile int*)nflag = 0;
+    return fail(RTK_ERR_NUMERIC, "an earlier solve on this device hit a numeric failure (non-finite iterate or "
+                                 "unrepairable Cholesky breakdown); its outputs are unreliable");
+  }
+  RTK_CK(cudaGraphLaunch(E.exec, st));
+  g_launches += E.launches;
+  return RTK_OK;
+}
+
 }  // namespace
 }  // namespace rtk
 
@@ -937,21 +1062,21 @@ int rtk_solve(const rtk_options* opt, const float* A, const int64_t* dims, int32
               size_t ws_bytes, void* stream, rtk_report* rep) {
   rtk_options o = {1, 1, 0.0, 0, 0, 0};
   if (opt) o = *opt;
-  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+  return rtk::solve_entry(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
 int rtk_rthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                 int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                 void* stream, rtk_report* rep) {
   rtk_options o = {0, 1, 0.0, 0, 0, 0};
-  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+  return rtk::solve_entry(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
 int rtk_rsthosvd(const float* A, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,
                  int32_t q, uint64_t seed, float* const* U, float* core, void* ws, size_t ws_bytes,
                  void* stream, rtk_report* rep) {
   rtk_options o = {1, 1, 0.0, 0, 0, 0};
-  return rtk::solve(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
+  return rtk::solve_entry(o, A, dims, d, ranks, p, q, seed, U, core, ws, ws_bytes, stream, rep);
 }
 
 size_t rtk_workspace_bytes(int32_t algo, const int64_t* dims, int32_t d, const int32_t* ranks, int32_t p,

@@ -1,0 +1,46 @@
+"""A/B of the library's own graph replay (rtk_api.cu solve_entry): RTK_GRAPH=0 (direct enqueue) vs the
+default (replay), alternating blocks of reps through the public API with reused outputs.
+python scripts/graph_ab2.py [c4] [reps] [rounds]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2506_04840_b200 as rt  # noqa: E402
+from workloads import CONFIGS, make_config_tensor_torch  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+c = CONFIGS[name]
+A = make_config_tensor_torch(name)
+seq = c["algo"] == "rsthosvd"
+out = rt.solve(A, c["ranks"], c["p"], c["q"], c["omega_seed"], sequential=seq)
+
+
+def timed(graph):
+    if graph:
+        os.environ.pop("RTK_GRAPH", None)
+    else:
+        os.environ["RTK_GRAPH"] = "0"
+    for _ in range(3):
+        rt.solve(A, c["ranks"], c["p"], c["q"], c["omega_seed"], sequential=seq, out=out)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        rt.solve(A, c["ranks"], c["p"], c["q"], c["omega_seed"], sequential=seq, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    return round(e0.elapsed_time(e1) / reps, 4)
+
+
+res = {"config": name, "direct": [], "graph": []}
+for _ in range(rounds):
+    res["direct"].append(timed(False))
+    res["graph"].append(timed(True))
+print(json.dumps(res))
