@@ -24,7 +24,8 @@
  * between calls except a per-thread error string, cached kernel attributes and,
  * per host thread and device, a small pool of internal streams and events (the
  * side stream of the deferred shift update and Alg. 3's per-mode streams, joined
- * back into `stream` before the call returns its work).  A ws shared by two
+ * back into `stream` before the call returns its work) and the CUDA graphs of
+ * repeated calls (REPEATED CALLS below).  A ws shared by two
  * calls must not be in use by both at once (ordinary stream ordering suffices).
  * If ws == NULL the call allocates (cudaMallocAsync) and frees its own
  * workspace on the stream.
@@ -51,12 +52,28 @@
  * l_k <= 64 takes the cluster small solver), Alg. A.2 and Alg. B.1 need l_k <= 64.
  *
  * STREAMING PATHS (chosen per mode, results equal up to rounding; rtk_options.path
- * forces one).  tcgen05 3xTF32 when l_k <= 64, the unfolding is a contiguous
- * column-major view (mode 1 of A, every Alg. 4 mode, since Alg. 4 writes each
- * shrunk unfolding contiguously) whose leading dimension is a multiple of 4 and
- * whose base is 16-byte aligned; then the fused single-HBM-pass engine when
- * additionally n_k <= 1024.  Strided unfoldings (Alg. 3 modes >= 2), l_k > 64 and
- * unaligned data use the FP32 FFMA tile kernels (bulk-copy row loads, no permute).
+ * forces one).  tcgen05 when l_k <= 64, the view is 16-byte aligned and
+ * its leading dimension a multiple of 4:
+ *   - contiguous views (mode 1 of A, every Alg. 4 mode, since Alg. 4 writes each shrunk
+ *     unfolding contiguously) with n_k > 256 and at least one 256-column pair-block per two
+ *     SM pairs: the CTA-pair engine (cta_group::2); its power steps use fp16 two-plane
+ *     operands (3xFP16) once max|M| of the unfolding is known, else 3xTF32;
+ *   - other contiguous views with n_k <= 1024: the one-CTA fused single-HBM-pass engine;
+ *   - Alg. 3's strided views (modes >= 2 of A): the one-CTA fused engine through 3-D TMA
+ *     tensor maps {p, i, s} (no permute copy);
+ *   - contiguous views with n_k > 1024: the two-kernel tcgen05 path.
+ * l_k > 64, unaligned data and views the engines do not take use the FP32 FFMA tile
+ * kernels (bulk-copy row loads, no permute).
+ *
+ * REPEATED CALLS (CUDA graphs).  rtk_solve / rtk_rthosvd / rtk_rsthosvd called again with
+ * IDENTICAL arguments (every pointer, extent, option, the seed, the device and every RTK_*
+ * environment variable) replay a CUDA graph of the first call's launch sequence: the second
+ * call of such a key captures it (on a private stream) and launches it on `stream`, later
+ * calls only launch it.  The graph reads the CURRENT contents of A and writes the same
+ * outputs, bit-identical to the direct path.  A graph exists only for arguments that passed
+ * every check once; the sticky RTK_ERR_NUMERIC check runs before every replay.  Not used when rep != NULL, ws == NULL, per-launch
+ * profiling is on, `stream` is being captured by the caller, or RTK_GRAPH=0; at most 16
+ * graphs are kept (least recently used evicted after a device synchronise).
  */
 #ifndef RTUCKER_H
 #define RTUCKER_H
