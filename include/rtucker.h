@@ -72,7 +72,7 @@
  * calls only launch it.  The graph reads the CURRENT contents of A and writes the same
  * outputs, bit-identical to the direct path.  A graph exists only for arguments that passed
  * every check once; the sticky RTK_ERR_NUMERIC check runs before every replay.  Not used when rep != NULL, ws == NULL, per-launch
- * profiling is on, `stream` is being captured by the caller, or RTK_GRAPH=0; at most 16
+ * profiling is on, `stream` is being captured by the caller, or RTK_GRAPH=0; at most 32
  * graphs are kept (least recently used evicted after a device synchronise).
  */
 #ifndef RTUCKER_H

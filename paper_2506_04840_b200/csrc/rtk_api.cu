@@ -991,7 +991,7 @@ int solve_entry(const rtk_options& o, const float* A, const int64_t* dims, int32
   for (size_t i = 0; i < cache.size(); ++i)
     if (cache[i].key == key) { idx = i; break; }
   if (idx == cache.size()) {
-    if (cache.size() >= 16) {   // evict the least recently used graph (no launch of it may be pending)
+    if (cache.size() >= 32) {   // evict the least recently used graph (no launch of it may be pending)
       if (cache.front().exec) {
         cudaDeviceSynchronize();
         cudaGraphExecDestroy(cache.front().exec);

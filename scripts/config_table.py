@@ -19,7 +19,12 @@ from workloads import CONFIGS, make_config_tensor, make_config_tensor_torch  # n
 
 
 def gpu_time(fn, A, c, reps=5, **kw):
-    fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"], **kw)
+    """Per call, synchronised (host enqueue latency included), after 4 warm-up calls: every call
+    allocates new outputs, so two output sets alternate and both keys are captured as CUDA graphs
+    before timing (rtk_api.cu solve_entry); then the back-to-back device time of 10 calls with the
+    graph replay and with RTK_GRAPH=0 (direct enqueue)."""
+    for _ in range(4):
+        out = fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"], **kw)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
@@ -29,12 +34,28 @@ def gpu_time(fn, A, c, reps=5, **kw):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    return float(np.median(ts)), out
+    b2b = {}
+    for mode in ("graph", "direct"):
+        if mode == "direct":
+            os.environ["RTK_GRAPH"] = "0"
+        core, U = out
+        for _ in range(3):
+            fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"], out=(core, U), **kw)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            fn(A, c["ranks"], c["p"], c["q"], c["omega_seed"], out=(core, U), **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        b2b[mode] = e0.elapsed_time(e1) / 10
+        os.environ.pop("RTK_GRAPH", None)
+    return float(np.median(ts)), b2b, out
 
 
-print("| config | algorithm | GPU ms / solve (median of 5) | RE GPU | RE oracle | rel. diff | oracle s (CPU, %d cores) |"
+print("| config | algorithm | GPU ms / solve (per call, synced, median of 5) | back-to-back ms (graph / direct) | RE GPU | RE oracle | rel. diff | oracle s (CPU, %d cores) |"
       % os.cpu_count())
-print("|---|---|---|---|---|---|---|")
+print("|---|---|---|---|---|---|---|---|")
 for name, c in CONFIGS.items():
     seq = c["algo"] == "rsthosvd"
     variants = [("Alg. 4" if seq else "Alg. 3", rt.rsthosvd if seq else rt.rthosvd,
@@ -48,7 +69,7 @@ for name, c in CONFIGS.items():
         a = make_config_tensor(name)
         A = torch.from_numpy(np.asfortranarray(a)).to("cuda")
     for label, gfn, ofn, kw in variants:
-        ms, (core, U) = gpu_time(gfn, A, c, **kw)
+        ms, b2b, (core, U) = gpu_time(gfn, A, c, **kw)
         if a is None:
             a = A.cpu().numpy()
         re_g = metrics.relative_error(a, core.cpu().numpy(), [u.cpu().numpy() for u in U])
@@ -56,5 +77,5 @@ for name, c in CONFIGS.items():
         orc = ofn(a, c["ranks"], c["p"], c["q"], c["omega_seed"])
         t_o = time.perf_counter() - t0
         re_o = metrics.relative_error(a, orc.core, orc.factors)
-        print(f"| {name} | {label} | {ms:.3f} | {re_g:.6e} | {re_o:.6e} | {abs(re_g - re_o) / re_o:.1e} | {t_o:.2f} |",
+        print(f"| {name} | {label} | {ms:.3f} | {b2b['graph']:.3f} / {b2b['direct']:.3f} | {re_g:.6e} | {re_o:.6e} | {abs(re_g - re_o) / re_o:.1e} | {t_o:.2f} |",
               flush=True)
