@@ -76,11 +76,14 @@ __global__ void __launch_bounds__(kRT) reduce_gram_kernel(const float* __restric
                                                          const double* __restrict__ Qd,
                                                          const double* __restrict__ alpha, int power,
                                                          double* __restrict__ Y, double* __restrict__ gpart,
-                                                         const int* __restrict__ stop, int gmode) {
+                                                         const int* __restrict__ stop, int gmode, int early) {
   // gmode 0: Y and the Gram partials; 1: Y only (a multi-GPU shard, before Y's all-reduce);
   // 2: the Gram partials of the (all-reduced) Y already in Y
   __shared__ double Ys[kRBr][kSL + 1];
   __shared__ double gps[kSL * (kSL + 1) / 2];   // this CTA's 8-row Gram (packed upper)
+  // early: let the step kernel's CTAs launch now (onto the SMs this grid leaves free) so their
+  // launch overlaps this reduction; they still wait for its completion in griddepcontrol.wait
+  if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   sm100::pdl_wait();   // the power step's Y partials
   if (stop && *(volatile const int*)stop) return;   // Alg. B.1 stopped this mode (uniform over the grid)
   const int tid = threadIdx.x;
@@ -2000,6 +2003,14 @@ int solve_cluster_size(int n) {
 
 size_t solve_gpart_doubles(int n, int l) { return (size_t)gram_blocks(n) * l * (l + 1) / 2; }
 
+// reduce_gram releases the step kernel at entry (its CTAs launch onto the SMs the reduction leaves
+// free and wait in griddepcontrol.wait): C4 1.511 -> 1.473 ms, C3 1.460 -> 1.433, C5 unchanged
+// (profiles/r2l_ab.txt).  RTK_RG_EARLY=0 keeps the implicit trigger at grid exit.
+static bool rg_early() {
+  const char* e = getenv("RTK_RG_EARLY");
+  return !(e && e[0] == '0');
+}
+
 cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, const int* stop, int gmode) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(gram_blocks(B.n) * kRGC, 1, 1);   // CTAs past n contribute zero rows
@@ -2020,7 +2031,7 @@ cudaError_t launch_reduce_gram2(const ModeBufs& B, bool power, cudaStream_t st, 
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, reduce_gram_kernel, (const float*)B.Ypart, B.G, B.ltot, B.n_rows, B.n,
                                      B.l, (const double*)B.Qd, (const double*)B.alpha, power ? 1 : 0, B.Y, B.gpart,
-                                     stop, gmode);
+                                     stop, gmode, rg_early() ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
