@@ -2,7 +2,9 @@
 algorithm (Alg. 3 / 4 / A.2), streaming path, shift on/off and sketch type, each checked with the
 north_star tolerances.  Prints one line per case and a summary; exits 1 on any failure.
 
-python scripts/parity_sweep.py [n_cases] [seed]
+python scripts/parity_sweep.py [n_cases] [seed] [big]
+"big": d = 3 with n_1 in [257, 1000] and up to 2e7 entries, tensor path only, so mode 1 (and often mode 2)
+runs on the CTA-pair engine (fp16 power steps, pair sketch / shrink), the fused sketch forced on at random.
 """
 import os
 import sys
@@ -17,18 +19,23 @@ from oracle import metrics, tucker  # noqa: E402
 from workloads import orthonormal_factor, tucker_tensor  # noqa: E402
 
 
-def case(rng):
-    d = int(rng.integers(2, 5))
-    budget = {2: 400000, 3: 2000000, 4: 1500000}[d]
+def case(rng, big=False):
+    d = 3 if big else int(rng.integers(2, 5))
+    budget = 20000000 if big else {2: 400000, 3: 2000000, 4: 1500000}[d]
     while True:
-        dims = [int(rng.integers(2, 700 if d == 2 else (220 if d == 3 else 48))) for _ in range(d)]
+        if big:
+            dims = [int(rng.integers(257, 1001)), int(rng.integers(8, 400)), int(rng.integers(8, 400))]
+            if rng.integers(0, 4) == 0:          # sometimes the long mode is not the first
+                dims = [dims[1], dims[0], dims[2]]
+        else:
+            dims = [int(rng.integers(2, 700 if d == 2 else (220 if d == 3 else 48))) for _ in range(d)]
         if int(np.prod(dims)) <= budget:
             break
     algo = ["t", "st", "a2"][int(rng.integers(0, 3))] if d > 1 else "st"
     p = int(rng.integers(0, 11))
     ranks = []
     for k, n in enumerate(dims):
-        ranks.append(int(rng.integers(1, max(2, min(n, 40)))))
+        ranks.append(int(rng.integers(1, max(2, min(n, 56 if big else 40)))))
     # respect l_k <= min(n_k, m_k) (m_k over the shrunk extents for ST / A.2)
     for _ in range(50):
         ok = True
@@ -56,20 +63,24 @@ def case(rng):
     else:
         return None
     q = int(rng.integers(1, 5))
-    path = ["ffma", "tc"][int(rng.integers(0, 2))]
+    path = "tc" if big else ["ffma", "tc"][int(rng.integers(0, 2))]
     shift = bool(rng.integers(0, 4) > 0)
     omega = int(rng.integers(0, 4)) if rng.integers(0, 3) == 0 else 0
-    return dict(dims=dims, ranks=ranks, p=p, q=q, algo=algo, path=path, shift=shift, omega=omega)
+    c = dict(dims=dims, ranks=ranks, p=p, q=q, algo=algo, path=path, shift=shift, omega=omega)
+    if big:
+        c["fused_sketch_min"] = 0 if rng.integers(0, 2) else None
+    return c
 
 
 def main():
     n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+    big = len(sys.argv) > 3 and sys.argv[3] == "big"
     fails = 0
     ties = 0
     done = 0
     while done < n_cases:
-        c = case(rng)
+        c = case(rng, big)
         if c is None:
             continue
         done += 1
@@ -78,6 +89,10 @@ def main():
         core = rng.standard_normal(cr) * np.exp(-0.3 * np.indices(cr).sum(axis=0))
         a = tucker_tensor(core, [orthonormal_factor(n, r, rng) for n, r in zip(dims, cr)], noise=1e-3, rng=rng)
         os.environ["RTK_PATH"] = c["path"]
+        if c.get("fused_sketch_min") is not None:
+            os.environ["RTK_FUSED_SKETCH_MIN"] = str(c["fused_sketch_min"])
+        else:
+            os.environ.pop("RTK_FUSED_SKETCH_MIN", None)
         A = torch.from_numpy(np.asfortranarray(a)).cuda()
         seq, variant = c["algo"] != "t", 1 if c["algo"] == "a2" else 0
         try:
