@@ -489,9 +489,9 @@ def test_sketch_type_parity(kind, algo, path, monkeypatch):
     ((1, 30, 20), (1, 4, 3), 0, 2),            # n_1 = 1 (a matrix in disguise)
     ((300, 90, 90), (70, 8, 6), 10, 2),        # l_1 = 80 > 64: the one-CTA Jacobi small solves
     ((4096, 9, 7), (6, 3, 2), 3, 1),           # n_k at the kernel limit (4096)
-    ((1152, 96, 40), (30, 12, 8), 10, 2),      # n_1 in (1024, 2048]: past the pair engine's four Y pair-tiles,
-    ((1280, 60, 50), (40, 10, 8), 10, 1),      #   the one-CTA cluster engine (the paper's Table 1 row counts)
-    ((2100, 40, 30), (20, 8, 6), 6, 2),        # n_1 > 2048: past the cluster engine too
+    ((1152, 96, 40), (30, 12, 8), 10, 2),      # n_1 > 1024: past both fused engines (four Y pair-tiles /
+    ((1280, 60, 50), (40, 10, 8), 10, 1),      #   two-CTA cluster), the two-kernel tcgen05 path (the paper's
+    ((2100, 40, 30), (20, 8, 6), 6, 2),        #   Table 1 row counts 1152 and 1280; 2100)
 ])
 def test_edge_shapes(seq, dims, ranks, p, q):
     rng = np.random.default_rng(sum(dims) + 3)
