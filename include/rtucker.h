@@ -64,6 +64,11 @@
  *   - contiguous views with n_k > 1024: the two-kernel tcgen05 path.
  * l_k > 64, unaligned data and views the engines do not take use the FP32 FFMA tile
  * kernels (bulk-copy row loads, no permute).
+ * ACCURACY NOTE.  The tcgen05 engines accumulate in the tensor core's fp32 accumulator, which
+ * rounds toward zero: on same-sign data a power step's Y comes out uniformly smaller by up to
+ * ~1e-4 relative at C5 size (mixed-sign data: ~1e-5), alpha by twice that; the column space
+ * (U_k, RE) is unaffected to first order.  path = 1 (FFMA tiles) has no such bias
+ * (profiles/r2m_rz_probe.md).
  *
  * REPEATED CALLS (CUDA graphs).  rtk_solve / rtk_rthosvd / rtk_rsthosvd called again with
  * IDENTICAL arguments (every pointer, extent, option, the seed, the device and every RTK_*
