@@ -114,6 +114,37 @@ def test_power_step_f16_pair_vs_fp64(n, m, l, scale, spread, monkeypatch):
     assert ew < TOL_EW["fused"], ew
 
 
+# Same-sign operands (no cancellation): the tensor core's fp32 accumulator rounds toward zero, so every
+# tcgen05 engine returns Y uniformly a little small, in proportion to the MMAs one accumulator receives
+# (profiles/r2m_rz_probe.md: 512 x 2e5 -> 5.0e-5 on 3xTF32, 2.5e-5 on the fp16 engine, 2.9e-5 one-CTA,
+# 1e-10 on the FFMA tiles).  Bounds = 2x the measured bias: a regression guard for the chain lengths, and
+# the reason alpha's tolerance (rtol 1e-3) is not tightened.  The reference is the plain definition in
+# float64 (numpy matmul of the same fp32 values).
+@pytest.mark.parametrize("engine,env,bound", [
+    ("3xTF32 pair", {"RTK_PATH": "tc", "RTK_PAIR": "1"}, 1.0e-4),
+    ("fp16 pair", {"RTK_PATH": "tc", "RTK_PAIR": "1", "RTK_POWER_F16": "1"}, 5.0e-5),
+    ("one-CTA fused", {"RTK_PATH": "tc", "RTK_PAIR": "0"}, 6.0e-5),
+    ("FFMA tiles", {"RTK_PATH": "ffma"}, 2.0e-6),
+])
+def test_power_step_same_sign_bias(engine, env, bound, monkeypatch):
+    torch = cuda_or_skip()
+    from paper_2506_04840_b200 import power_step
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n, m, l = 512, 200000, 60
+    rng = np.random.default_rng(512)
+    M = np.abs(rng.standard_normal((n, m))).astype(np.float32)
+    Q = (np.abs(rng.standard_normal((n, l))) / np.sqrt(n)).astype(np.float32)
+    Md = torch.from_numpy(np.asfortranarray(M)).cuda()
+    Y = power_step(Md, torch.from_numpy(Q).cuda()).cpu().numpy()
+    ref = M.astype(np.float64) @ (M.astype(np.float64).T @ Q.astype(np.float64))
+    rel = (Y - ref) / ref
+    print(f"{engine}: mean {rel.mean():+.3e} max |rel| {np.abs(rel).max():.3e}")
+    assert float(np.abs(rel).max()) < bound, (engine, float(rel.mean()), float(np.abs(rel).max()))
+    if "ffma" not in env.get("RTK_PATH", ""):
+        assert rel.mean() < 0 and np.abs(rel).max() < 1.5 * abs(rel.mean())    # a uniform shrink, not noise
+
+
 def test_power_step_padded_leading_dimension():
     torch = cuda_or_skip()
     from paper_2506_04840_b200 import power_step
